@@ -1,0 +1,187 @@
+/*
+ * jigsaw_sm100.h — C ABI of libjigsaw_sm100.so, the sm_100a (B200) kernels behind
+ * the WeatherMixer training step and its Jigsaw-sharded layers.
+ *
+ * The reference (`jigsaw` 0.1.0, /root/reference/pkg/src/jigsaw) is pure numpy and has
+ * no FFI; its operator boundary is the Python functions in tensor.py / parallel.py /
+ * model.py. Every entry point below replaces one of those operators (cited per entry),
+ * and the Python host package `paper_2507_05753_b200` binds them with ctypes
+ * (INTEGRATION.md shows the binding a maintainer would add to the reference).
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless stated otherwise; sizes are element counts.
+ *   - Every call is asynchronous on the given cudaStream_t (passed as void*), allocates
+ *     nothing and never synchronises the host.
+ *   - Return value: 0 = OK, JG_ERR_SHAPE = shape/dtype/alignment error (Python maps it to
+ *     ShapeError, the reference's tensor.py:23), JG_ERR_CUDA = launch/driver error
+ *     (RuntimeError). jg_last_error() returns a thread-local message naming the problem.
+ */
+#ifndef JIGSAW_SM100_H
+#define JIGSAW_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#pragma GCC visibility push(default)
+
+#define JG_OK 0
+#define JG_ERR_SHAPE 1
+#define JG_ERR_CUDA 2
+
+/* element types */
+#define JG_F32 0
+#define JG_BF16 1
+
+/* operand storage order for jg_gemm (tensor.py:27-33 MatmulMode is expressed through these) */
+#define JG_KMAJOR 0  /* operand stored [rows(M or N)][K], K contiguous              */
+#define JG_MNMAJOR 1 /* operand stored [K][rows(M or N)], the M (or N) axis contiguous */
+
+/* arithmetic of jg_gemm */
+#define JG_MATH_BF16 0   /* bf16 operands, fp32 accumulate in TMEM (tcgen05 kind::f16) */
+#define JG_MATH_TF32X3 1 /* fp32 operands split hi/lo, 3 tcgen05 kind::tf32 passes   */
+
+/* epilogue flags for jg_gemm */
+#define JG_EPI_ACCUM 1u     /* D += result (fp32 D): weight-grad accumulation, parallel.py:490-493 */
+#define JG_EPI_BIAS_COL 2u  /* result += bias[col]  (parallel.py:524-525)                          */
+#define JG_EPI_BIAS_ROW 4u  /* result += bias[row]  (weight-first tok2, parallel.py:522-523)       */
+#define JG_EPI_RESID 8u     /* result += resid[row,col] (residual add, model.py:274,280)           */
+#define JG_EPI_GELU_FWD 16u /* D = result (pre-activation), D2 = gelu(result)  (tensor.py:75-77)   */
+#define JG_EPI_GELU_BWD 32u /* result *= gelu'(pre[row,col])                   (tensor.py:80-84)   */
+#define JG_EPI_COPY_D2 64u  /* D2 = result as well (e.g. bf16 operand copy of an fp32 output)     */
+#define JG_EPI_STATS 128u   /* stats[row] += (sum_col result, sum_col result^2)  (model.py:234)     */
+
+/*
+ * jg_gemm — one (batched) GEMM with a fused epilogue.
+ * Replaces tensor.matmul (tensor.py:59-72) as called by MpContext._mm (parallel.py:65-69),
+ * plus the bias add / GELU / residual / layer-norm-moment elementwise work that follows
+ * each call in ShardedLinear.forward (parallel.py:515-526) and MixerBlock (model.py:268-297).
+ *
+ * Logical problem, per batch index b:   R[b] = sum_k A[b](m,k) * B[b](n,k)    (m < M, n < N)
+ *   A element (m,k) lives at a[b*a_bstride + m*lda + k]   when a_major == JG_KMAJOR
+ *                            a[b*a_bstride + k*lda + m]   when a_major == JG_MNMAJOR
+ *   (same for B with n in place of m). NT = (K,K), NN = (K,MN) for B, TN = (MN,MN).
+ * reduce_batch != 0: R = sum_b R[b] (weight gradients summed over the batch, parallel.py:552-556),
+ *   written to batch slot 0 of D.
+ * a_bstride == 0 (or b_bstride == 0) broadcasts that operand over the batch.
+ * For JG_MATH_TF32X3 the caller passes the fp32 hi/lo split of each operand (jg_split_tf32_2d),
+ *   both K-major: a/b = hi parts, a_lo/b_lo = lo parts;  R = Ahi*Bhi + Ahi*Blo + Alo*Bhi.
+ * The epilogue then applies, in order: alpha*R, +bias, +resid, (+D if ACCUM), GELU fwd/bwd,
+ * stores D (d_type) and D2 (d2_type), and accumulates row moments.
+ */
+typedef struct jg_gemm_desc {
+  int64_t m, n, k, batch;
+  int32_t math;          /* JG_MATH_* */
+  int32_t reduce_batch;  /* 0/1 */
+  const void* a; const void* a_lo; int64_t lda, a_bstride; int32_t a_major;
+  const void* b; const void* b_lo; int64_t ldb, b_bstride; int32_t b_major;
+  uint32_t epi;          /* JG_EPI_* */
+  float alpha;
+  void* d;  int64_t ldd,  d_bstride;  int32_t d_type;
+  void* d2; int64_t ldd2, d2_bstride; int32_t d2_type;
+  const float* bias; int64_t bias_bstride;
+  const float* resid; int64_t ldr, r_bstride;
+  const void* pre; int64_t ldp, p_bstride; int32_t pre_type;
+  float* stats; int64_t stats_bstride;   /* [rows][2] fp32, must be zeroed by the caller */
+} jg_gemm_desc;
+
+int jg_gemm(const jg_gemm_desc* desc, void* stream);
+
+/* Split fp32 x into tf32-exact hi (low 13 mantissa bits cleared) and lo = x - hi. */
+int jg_split_tf32(const float* x, float* hi, float* lo, int64_t n, void* stream);
+
+/* 2-D split into K-major 3xTF32 operands: x[b][rows][cols] (row stride ldx, batch stride
+ * x_bstride) -> hi/lo [b][transpose ? cols : rows][ldo], zero-padded up to ldo, so that
+ * MN-major fp32 operands become K-major and any K becomes a 16-byte multiple. */
+int jg_split_tf32_2d(const float* x, int64_t rows, int64_t cols, int64_t ldx, int64_t batch, int64_t x_bstride,
+                     int32_t transpose, float* hi, float* lo, int64_t ldo, void* stream);
+
+/* Elementwise cast fp32 -> bf16 (round to nearest even). */
+int jg_cast_bf16(const float* x, void* y_bf16, int64_t n, void* stream);
+
+/* GELU forward / backward as standalone ops (tensor.py:75-84). dtype = JG_F32 or JG_BF16 for
+ * x/y/g; the math is fp32. y = gelu(x);  dx = g * (Phi(x) + x*phi(x)). */
+int jg_gelu_fwd(const void* x, void* y, int32_t dtype, int64_t n, void* stream);
+int jg_gelu_bwd(const void* x, const void* g, void* dx, int32_t dtype, int64_t n, void* stream);
+
+/*
+ * Layer norm over the last axis, possibly split across ranks (ShardedLayerNorm,
+ * model.py:200-250; serial twin tensor.py:87-123).  Rows = R, local width = C,
+ * normalised width = c_total (C * column-split ways).  Row moments are exchanged between
+ * the two phases by the caller (an NCCL all-reduce over the row group) when C < c_total.
+ */
+/* phase 0 (forward): stats[r] += (sum x, sum x^2) over the local columns. */
+int jg_ln_moments(const float* x, float* stats, int64_t rows, int64_t cols, int64_t ldx, void* stream);
+/* phase 1 (forward): y = gamma * (x - mean) * inv_std + beta ; saves (mean, inv_std) per row. */
+int jg_ln_apply(const float* x, const float* stats, const float* gamma, const float* beta,
+                void* y, int32_t y_type, float* mean_rstd, int64_t rows, int64_t cols,
+                int64_t c_total, float eps, void* stream);
+/* backward phase 0: bstats[r] += (sum h, sum h*xhat) with h = g*gamma, xhat from x & mean_rstd. */
+int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const float* mean_rstd,
+                      float* bstats, int64_t rows, int64_t cols, void* stream);
+/* backward phase 1: dx = inv_std*(h - sum_h/c_total - xhat*sum_hx/c_total);
+ * out = (resid ? resid : 0) + dx  (fp32), out_bf16 optional copy;
+ * dgamma[c] += sum_r g*xhat ; dbeta[c] += sum_r g ; rowsum_out[r] += sum_c out (optional). */
+int jg_ln_bwd_apply(const float* x, const float* g, const float* gamma, const float* mean_rstd,
+                    const float* bstats, const float* resid, float* out, void* out_bf16,
+                    float* dgamma, float* dbeta, float* rowsum_out,
+                    int64_t rows, int64_t cols, int64_t c_total, void* stream);
+
+/* Column sums (bias gradients, parallel.py:548,559-561): out[c] += sum_r x[r*ld + c];
+ * Row sums (row-bias gradient of weight-first tok2, parallel.py:536): out[r] += sum_c x[r*ld+c]. */
+int jg_colsum(const void* x, int32_t x_type, float* out, int64_t rows, int64_t cols, int64_t ldx, void* stream);
+int jg_rowsum(const void* x, int32_t x_type, float* out, int64_t rows, int64_t cols, int64_t ldx, void* stream);
+
+/* patchify / unpatchify (tensor.py:126-151): x [B, lat, lon, C] <-> tokens [B, T, C*p_lat*p_lon],
+ * channel-major features, row-major tokens. x_type/t_type = JG_F32 or JG_BF16. */
+int jg_patchify(const float* x, void* tokens, int32_t t_type, int64_t batch, int64_t lat, int64_t lon,
+                int64_t chans, int64_t p_lat, int64_t p_lon, void* stream);
+int jg_unpatchify(const float* tokens, float* x, int64_t batch, int64_t lat, int64_t lon,
+                  int64_t chans, int64_t p_lat, int64_t p_lon, void* stream);
+
+/*
+ * Fused decoder tail + loss (model.py:420-438 blend forward/backward; SPEC.md:396-413
+ * lat-weighted MSE).  dec_tok = decoder output in token layout [B, T, F] (fp32).
+ *   decoded = unpatchify(dec_tok); out = w*decoded + (1-w)*x                      (model.py:424)
+ *   loss_partial += sum lat_w[lat] * var_w[c] * (out - target)^2 * inv_count
+ *   g_out = 2 * lat_w * var_w * (out - target) * inv_count * loss_scale
+ *   g_blend[c] += sum g_out * (decoded - x)                                      (model.py:437)
+ *   g_dec_tok = patchify(g_out * w)  written as fp32 and/or bf16                  (model.py:438-439)
+ * out / g_dec_f32 / g_dec_bf16 may be NULL. loss_sum is one fp32 scalar (pre-zeroed).
+ * g_out_ext (optional, [B,lat,lon,C] fp32): when non-NULL it REPLACES the MSE gradient
+ * (the reference's model.backward(g_out) entry point, model.py:428).
+ */
+int jg_blend_loss(const float* dec_tok, const float* x, const float* target, const float* blend_w,
+                  const float* lat_w, const float* var_w, const float* g_out_ext,
+                  float* out, float* loss_sum, float* g_blend, float* g_dec_f32, void* g_dec_bf16,
+                  int64_t batch, int64_t lat, int64_t lon, int64_t chans, int64_t p_lat, int64_t p_lon,
+                  float inv_count, float loss_scale, void* stream);
+
+/*
+ * Fused Adam over one flat fp32 parameter range (bias-corrected,
+ * p -= lr * mhat / (sqrt(vhat) + eps)); writes the bf16 operand copy when p_bf16 != NULL.
+ * The step counter t (>= 1) is read from device memory so a captured CUDA graph replays
+ * correctly; *grad_scale_dev (NULL = 1.0) multiplies g first (global-norm clipping,
+ * SPEC.md:473-481).
+ */
+int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n,
+            float lr, float beta1, float beta2, float eps, const int32_t* step_dev,
+            const float* grad_scale_dev, void* stream);
+/* *counter += 1 on the device (advances the Adam step inside a graph). */
+int jg_step_increment(int32_t* counter, void* stream);
+
+/* Sum of squares of x (fp32) added into out[0] (global grad norm). */
+int jg_sqnorm(const float* x, int64_t n, float* out, void* stream);
+
+/* Introspection. */
+const char* jg_version(void);
+const char* jg_last_error(void);
+/* number of kernels launched by this library since load (evidence counter for bench.py). */
+int64_t jg_launch_count(void);
+
+#pragma GCC visibility pop
+#ifdef __cplusplus
+}
+#endif
+#endif /* JIGSAW_SM100_H */

@@ -1,0 +1,59 @@
+"""Build libjigsaw_sm100.so in-tree with nvcc for sm_100a (B200).
+
+Usage: python -m paper_2507_05753_b200.csrc.build [--verbose]
+The .so lands next to this file's package (paper_2507_05753_b200/libjigsaw_sm100.so) so it
+travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+PKG = HERE.parent
+ROOT = PKG.parent
+SOURCES = ["jg_api.cu", "jg_gemm.cu", "jg_rowwise.cu"]
+OUT = PKG / "libjigsaw_sm100.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    "--expt-relaxed-constexpr",
+    f"-I{ROOT / 'include'}",
+]
+
+
+def _stale() -> bool:
+    if not OUT.exists():
+        return True
+    t = OUT.stat().st_mtime
+    deps = [HERE / s for s in SOURCES] + list(HERE.glob("*.cuh")) + [ROOT / "include" / "jigsaw_sm100.h", Path(__file__)]
+    return any(d.stat().st_mtime > t for d in deps if d.exists())
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    if not force and not _stale():
+        return OUT
+    objs = []
+    for src in SOURCES:
+        obj = HERE / (Path(src).stem + ".o")
+        cmd = [NVCC, *FLAGS, "-c", str(HERE / src), "-o", str(obj)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        objs.append(str(obj))
+    tmp = OUT.with_suffix(".so.tmp")
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs, "-lcudart"],
+                   check=True)
+    os.replace(tmp, OUT)
+    for o in objs:
+        os.unlink(o)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose="--verbose" in sys.argv, force=True))

@@ -1,0 +1,496 @@
+// jg_gemm.cu — persistent, warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+// Replaces tensor.matmul (reference tensor.py:59-72) as used by every Jigsaw primitive
+// (parallel.py:107-353) and fuses the elementwise tails of ShardedLinear / MixerBlock
+// (bias parallel.py:521-525, GELU tensor.py:75-84, residual model.py:274/280, layer-norm
+// row moments model.py:234) into the accumulator read-out.
+//
+// Structure (one CTA per SM, persistent over output tiles of 128 x BN):
+//   warp 0 lane 0 : TMA producer — fills a STAGES-deep ring of (A,B) K-slices in smem,
+//                   128B-swizzled, completion counted on full[] mbarriers.
+//   warp 1 lane 0 : MMA issuer — 4 x tcgen05.mma per K-slice into a TMEM accumulator
+//                   (double-buffered: 2 x BN fp32 columns), frees smem via tcgen05.commit.
+//   warp 2        : TMEM allocator.
+//   warps 4..7    : epilogue — tcgen05.ld 32 lanes x 32 columns per step (thread == row),
+//                   applies bias / residual / GELU / GELU' / accumulate / row moments,
+//                   stores fp32 and/or bf16; releases the TMEM buffer to the MMA warp.
+// Operands may be K-major or MN-major (the NN / NT / TN modes of tensor.py:27-33), are
+// loaded with 3-D TMA (batch as the 3rd dimension) and may be summed over the batch
+// (weight gradients, parallel.py:552-556) or over up to three K segments (3xTF32 split).
+#include "jg_common.cuh"
+#include <cudaTypedefs.h>
+#include <mutex>
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int NUM_THREADS = 256;
+constexpr int SMEM_BUDGET = 196 * 1024;
+
+struct GemmParams {
+  CUtensorMap tma_a[3];
+  CUtensorMap tma_b[3];
+  int nseg;
+  int m, n, k;
+  int batch;
+  int reduce_batch;
+  int a_mn, b_mn;          // operand majors (1 = MN-major)
+  int a_batched, b_batched;
+  int num_kb;              // K blocks per (segment, batch)
+  int m_tiles, n_tiles;
+  int num_tiles;
+  // epilogue
+  uint32_t epi;
+  float alpha;
+  void* d; int64_t ldd, d_bs; int d_bf16;
+  void* d2; int64_t ldd2, d2_bs; int d2_bf16;
+  const float* bias; int64_t bias_bs;
+  const float* resid; int64_t ldr, r_bs;
+  const void* pre; int64_t ldp, p_bs; int pre_bf16;
+  float* stats; int64_t stats_bs;
+};
+
+template <int BN, bool TF32>
+struct Cfg {
+  static constexpr int ESIZE = TF32 ? 4 : 2;
+  static constexpr int BK = 128 / ESIZE;           // one 128-byte swizzle atom of K
+  static constexpr int UMMA_K = TF32 ? 8 : 16;     // 32 bytes of K per instruction
+  static constexpr int ATOM = 128 / ESIZE;         // elements per 128B row of an MN-major box
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
+  static constexpr int TMEM_COLS = 2 * BN;          // double-buffered fp32 accumulator
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t IDESC_BASE =
+      (1u << 4)                                    // D format: f32
+      | ((TF32 ? 2u : 1u) << 7)                    // A format: tf32 / bf16
+      | ((TF32 ? 2u : 1u) << 10)                   // B format
+      | (static_cast<uint32_t>(BN >> 3) << 17)     // N
+      | (static_cast<uint32_t>(BM >> 4) << 24);    // M
+};
+
+template <int BN, bool TF32>
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
+  using C = Cfg<BN, TF32>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.nseg; ++s) {
+      jgd::tma_prefetch_desc(&p.tma_a[s]);
+      jgd::tma_prefetch_desc(&p.tma_b[s]);
+    }
+    for (int s = 0; s < C::STAGES; ++s) {
+      jgd::mbar_init(&full[s], 1);
+      jgd::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      jgd::mbar_init(&tfull[s], 1);
+      jgd::mbar_init(&tempty[s], 4);
+    }
+    jgd::mbar_fence_init();
+  }
+  if (warp == 2) jgd::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  jgd::tc_fence_before();
+  __syncthreads();
+  jgd::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int kb_batches = p.reduce_batch ? p.batch : 1;
+  const int kb_per_tile = p.nseg * kb_batches * p.num_kb;
+  const int tiles_per_batch = p.m_tiles * p.n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    // ===================== TMA producer =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
+      const int rem = tile - tb * tiles_per_batch;
+      const int m0 = (rem / p.n_tiles) * BM;
+      const int n0 = (rem % p.n_tiles) * BN;
+      for (int seg = 0; seg < p.nseg; ++seg) {
+        for (int bb = 0; bb < kb_batches; ++bb) {
+          const int b = p.reduce_batch ? bb : tb;
+          const int ba = p.a_batched ? b : 0;
+          const int bbz = p.b_batched ? b : 0;
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            jgd::mbar_wait(&empty[stage], phase ^ 1);
+            jgd::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            const int k0 = kb * C::BK;
+            uint8_t* sa = smem_a + stage * C::A_BYTES;
+            uint8_t* sb = smem_b + stage * C::B_BYTES;
+            if (p.a_mn) {
+#pragma unroll
+              for (int j = 0; j < BM / C::ATOM; ++j)
+                jgd::tma_load_3d(sa + j * (C::BK * 128), &p.tma_a[seg], &full[stage], m0 + j * C::ATOM, k0, ba);
+            } else {
+              jgd::tma_load_3d(sa, &p.tma_a[seg], &full[stage], k0, m0, ba);
+            }
+            if (p.b_mn) {
+#pragma unroll
+              for (int j = 0; j < BN / C::ATOM; ++j)
+                jgd::tma_load_3d(sb + j * (C::BK * 128), &p.tma_b[seg], &full[stage], n0 + j * C::ATOM, k0, bbz);
+            } else {
+              jgd::tma_load_3d(sb, &p.tma_b[seg], &full[stage], k0, n0, bbz);
+            }
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ===================== MMA issuer =====================
+    const uint32_t idesc = C::IDESC_BASE | (static_cast<uint32_t>(p.a_mn) << 15) | (static_cast<uint32_t>(p.b_mn) << 16);
+    // K-major: SBO = 8 rows * 128B, per-instruction K step = 32 bytes inside the swizzle atom.
+    // MN-major: LBO = one (ATOM x BK) box, SBO = 8 K-rows * 128B, K step = UMMA_K rows * 128B.
+    const uint32_t a_lbo = p.a_mn ? C::BK * 128 : 16, b_lbo = p.b_mn ? C::BK * 128 : 16;
+    const uint32_t a_kstep = p.a_mn ? C::UMMA_K * 128 : 32, b_kstep = p.b_mn ? C::UMMA_K * 128 : 32;
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      jgd::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      jgd::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+      for (int i = 0; i < kb_per_tile; ++i) {
+        jgd::mbar_wait(&full[stage], phase);
+        jgd::tc_fence_after();
+        const uint32_t sa = jgd::smem_u32(smem_a + stage * C::A_BYTES);
+        const uint32_t sb = jgd::smem_u32(smem_b + stage * C::B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
+          const uint64_t ad = jgd::make_sdesc(sa + kk * a_kstep, a_lbo, 1024);
+          const uint64_t bd = jgd::make_sdesc(sb + kk * b_kstep, b_lbo, 1024);
+          if (TF32)
+            jgd::umma_tf32(d_tmem, ad, bd, idesc, (i | kk) != 0);
+          else
+            jgd::umma_bf16(d_tmem, ad, bd, idesc, (i | kk) != 0);
+        }
+        jgd::umma_commit(&empty[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      jgd::umma_commit(&tfull[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t epi = p.epi;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
+      const int rem = tile - tb * tiles_per_batch;
+      const int m0 = (rem / p.n_tiles) * BM;
+      const int n0 = (rem % p.n_tiles) * BN;
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < p.m;
+      jgd::mbar_wait(&tfull[acc], acc_phase);
+      jgd::tc_fence_after();
+
+      const int64_t drow = tb * p.d_bs + static_cast<int64_t>(row) * p.ldd;
+      const int64_t d2row = tb * p.d2_bs + static_cast<int64_t>(row) * p.ldd2;
+      const int64_t rrow = tb * p.r_bs + static_cast<int64_t>(row) * p.ldr;
+      const int64_t prow = tb * p.p_bs + static_cast<int64_t>(row) * p.ldp;
+      float rbias = 0.f;
+      if ((epi & JG_EPI_BIAS_ROW) && row_ok) rbias = p.bias[tb * p.bias_bs + row];
+      float s1 = 0.f, s2 = 0.f;
+
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = n0 + c * 32;
+        if (col0 >= p.n) break;  // warp-uniform
+        float v[32];
+        jgd::tmem_ld32(tmem_base + static_cast<uint32_t>(acc * BN + c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
+        if (!row_ok) continue;
+        const bool full_chunk = col0 + 32 <= p.n;
+        const int ncol = full_chunk ? 32 : p.n - col0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+        if (epi & JG_EPI_BIAS_COL) {
+          const float* bp = p.bias + tb * p.bias_bs + col0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += (j < ncol) ? __ldg(bp + j) : 0.f;
+        }
+        if (epi & JG_EPI_BIAS_ROW) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += rbias;
+        }
+        if (epi & JG_EPI_RESID) {
+          if (full_chunk) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float t[8];
+              jgd::load8(p.resid, rrow + col0 + g * 8, false, t);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[g * 8 + j] += t[j];
+            }
+          } else {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncol) v[j] += p.resid[rrow + col0 + j];
+          }
+        }
+        if (epi & JG_EPI_GELU_BWD) {
+          if (full_chunk) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float t[8];
+              jgd::load8(p.pre, prow + col0 + g * 8, p.pre_bf16, t);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[g * 8 + j] *= jgd::gelu_grad_f(t[j]);
+            }
+          } else {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncol) v[j] *= jgd::gelu_grad_f(jgd::load1(p.pre, prow + col0 + j, p.pre_bf16));
+          }
+        }
+        if (epi & JG_EPI_ACCUM) {
+          if (full_chunk) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float t[8];
+              jgd::load8(p.d, drow + col0 + g * 8, false, t);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[g * 8 + j] += t[j];
+            }
+          } else {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncol) v[j] += reinterpret_cast<const float*>(p.d)[drow + col0 + j];
+          }
+        }
+        if (epi & JG_EPI_STATS) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = (j < ncol) ? v[j] : 0.f;
+            s1 += x;
+            s2 += x * x;
+          }
+        }
+        // primary output
+        if (p.d != nullptr) {
+          if (full_chunk) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) jgd::store8(p.d, drow + col0 + g * 8, p.d_bf16, v + g * 8);
+          } else {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncol) jgd::store1(p.d, drow + col0 + j, p.d_bf16, v[j]);
+          }
+        }
+        // secondary output: gelu(result) or a plain copy
+        if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
+          if (epi & JG_EPI_GELU_FWD) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = jgd::gelu_f(v[j]);
+          }
+          if (full_chunk) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) jgd::store8(p.d2, d2row + col0 + g * 8, p.d2_bf16, v + g * 8);
+          } else {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncol) jgd::store1(p.d2, d2row + col0 + j, p.d2_bf16, v[j]);
+          }
+        }
+      }
+      if ((epi & JG_EPI_STATS) && row_ok) {
+        float* sp = p.stats + tb * p.stats_bs + static_cast<int64_t>(row) * 2;
+        atomicAdd(sp, s1);
+        atomicAdd(sp + 1, s2);
+      }
+      jgd::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) jgd::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    jgd::tc_fence_after();
+    jgd::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// Operand map. K-major: dims (K, rows, batch), box (BK, rows_box). MN-major: dims (rows, K, batch),
+// box (ATOM, BK). rows = M or N extent.
+int make_operand_map(CUtensorMap* map, const void* ptr, bool tf32, bool mn_major, int64_t rows, int64_t k,
+                     int64_t ld, int64_t bstride, int64_t batch, int box_rows) {
+  const int esize = tf32 ? 4 : 2;
+  const int atom = 128 / esize;
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3], estr[3] = {1, 1, 1};
+  if (mn_major) {
+    dims[0] = rows; dims[1] = k;
+    box[0] = atom; box[1] = atom;  // BK == ATOM
+  } else {
+    dims[0] = k; dims[1] = rows;
+    box[0] = atom; box[1] = box_rows;
+  }
+  dims[2] = batch;
+  box[2] = 1;
+  strides[0] = static_cast<cuuint64_t>(ld) * esize;
+  strides[1] = static_cast<cuuint64_t>(batch > 1 ? bstride : ld * (mn_major ? k : rows)) * esize;
+  if (strides[1] == 0 || strides[1] % 16) strides[1] = ((strides[0] * dims[1] + 15) / 16) * 16;
+  auto fn = encode_fn();
+  if (!fn) {
+    jg::set_error("cuTensorMapEncodeTiled unavailable (driver entry point lookup failed)");
+    return JG_ERR_CUDA;
+  }
+  CUresult r = fn(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d): rows=%lld k=%lld ld=%lld", (int)r,
+             (long long)rows, (long long)k, (long long)ld);
+    return jg::shape_error(buf);
+  }
+  return JG_OK;
+}
+
+template <int BN, bool TF32>
+int launch(GemmParams& p, cudaStream_t stream) {
+  using C = Cfg<BN, TF32>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    C::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return jg::cuda_check(attr_err, "cudaFuncSetAttribute(gemm)");
+  const int grid = p.num_tiles < jg::num_sms() ? p.num_tiles : jg::num_sms();
+  gemm_kernel<BN, TF32><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(p);
+  JG_LAUNCH_CHECK("gemm_kernel");
+  return JG_OK;
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  JG_SHAPE_CHECK(g != nullptr, "jg_gemm: null descriptor");
+  JG_SHAPE_CHECK(g->m > 0 && g->n > 0 && g->k > 0 && g->batch > 0, "jg_gemm: empty problem m=%lld n=%lld k=%lld batch=%lld",
+                 (long long)g->m, (long long)g->n, (long long)g->k, (long long)g->batch);
+  JG_SHAPE_CHECK(g->m < (1ll << 31) && g->n < (1ll << 31) && g->k < (1ll << 31), "jg_gemm: dimension too large");
+  const bool tf32 = g->math == JG_MATH_TF32X3;
+  JG_SHAPE_CHECK(g->math == JG_MATH_BF16 || tf32, "jg_gemm: unknown math %d", g->math);
+  const int esize = tf32 ? 4 : 2;
+  JG_SHAPE_CHECK(g->a && g->b && aligned16(g->a) && aligned16(g->b), "jg_gemm: operands must be 16-byte aligned");
+  JG_SHAPE_CHECK((g->lda * esize) % 16 == 0 && (g->ldb * esize) % 16 == 0,
+                 "jg_gemm: operand leading dims (%lld, %lld) must be multiples of %d elements", (long long)g->lda,
+                 (long long)g->ldb, 16 / esize);
+  JG_SHAPE_CHECK((g->a_bstride * esize) % 16 == 0 && (g->b_bstride * esize) % 16 == 0,
+                 "jg_gemm: operand batch strides must be multiples of 16 bytes");
+  JG_SHAPE_CHECK(g->lda >= (g->a_major == JG_MNMAJOR ? g->m : g->k), "jg_gemm: lda too small");
+  JG_SHAPE_CHECK(g->ldb >= (g->b_major == JG_MNMAJOR ? g->n : g->k), "jg_gemm: ldb too small");
+  if (tf32) {
+    JG_SHAPE_CHECK(g->a_lo && g->b_lo && aligned16(g->a_lo) && aligned16(g->b_lo), "jg_gemm: tf32x3 needs lo parts");
+    JG_SHAPE_CHECK(g->a_major == JG_KMAJOR && g->b_major == JG_KMAJOR,
+                   "jg_gemm: tf32x3 operands must be K-major (jg_split_tf32_2d transposes)");
+  }
+
+  const uint32_t epi = g->epi;
+  auto out_ok = [](const void* ptr, int64_t ld, int type) {
+    const int es = type == JG_BF16 ? 2 : 4;
+    return aligned16(ptr) && (ld * es) % 16 == 0;
+  };
+  JG_SHAPE_CHECK(g->d == nullptr || out_ok(g->d, g->ldd, g->d_type), "jg_gemm: D must be 16B aligned with ld %% 16B == 0");
+  JG_SHAPE_CHECK(!(epi & JG_EPI_ACCUM) || (g->d && g->d_type == JG_F32), "jg_gemm: ACCUM needs an fp32 D");
+  JG_SHAPE_CHECK(!(epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) || (g->d2 && out_ok(g->d2, g->ldd2, g->d2_type)),
+                 "jg_gemm: GELU_FWD/COPY_D2 need an aligned D2");
+  JG_SHAPE_CHECK(!(epi & (JG_EPI_BIAS_COL | JG_EPI_BIAS_ROW)) || g->bias, "jg_gemm: bias flag without bias");
+  JG_SHAPE_CHECK(!(epi & JG_EPI_RESID) || (g->resid && out_ok(g->resid, g->ldr, JG_F32)), "jg_gemm: bad resid");
+  JG_SHAPE_CHECK(!(epi & JG_EPI_GELU_BWD) || (g->pre && out_ok(g->pre, g->ldp, g->pre_type)), "jg_gemm: bad pre");
+  JG_SHAPE_CHECK(!(epi & JG_EPI_STATS) || g->stats, "jg_gemm: STATS without stats buffer");
+
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.m = static_cast<int>(g->m);
+  p.n = static_cast<int>(g->n);
+  p.k = static_cast<int>(g->k);
+  p.batch = static_cast<int>(g->batch);
+  p.reduce_batch = g->reduce_batch ? 1 : 0;
+  p.a_mn = g->a_major == JG_MNMAJOR;
+  p.b_mn = g->b_major == JG_MNMAJOR;
+  p.a_batched = g->batch > 1 && g->a_bstride != 0;
+  p.b_batched = g->batch > 1 && g->b_bstride != 0;
+  const int bk = 128 / esize;
+  p.num_kb = static_cast<int>((g->k + bk - 1) / bk);
+
+  // tile width: the widest N tile that still gives at least one full wave of tiles
+  const int64_t out_batches = p.reduce_batch ? 1 : g->batch;
+  const int64_t mt = (g->m + BM - 1) / BM;
+  int bn = 256;
+  if (g->n <= 64) bn = 64;
+  else if (g->n <= 128) bn = 128;
+  else {
+    const int64_t t256 = mt * ((g->n + 255) / 256) * out_batches;
+    if (t256 < jg::num_sms()) bn = 128;
+  }
+  p.m_tiles = static_cast<int>(mt);
+  p.n_tiles = static_cast<int>((g->n + bn - 1) / bn);
+  const int64_t nt = static_cast<int64_t>(p.m_tiles) * p.n_tiles * out_batches;
+  JG_SHAPE_CHECK(nt < (1ll << 31), "jg_gemm: too many tiles");
+  p.num_tiles = static_cast<int>(nt);
+
+  p.nseg = tf32 ? 3 : 1;
+  const void* as[3] = {g->a, g->a, g->a_lo};
+  const void* bs[3] = {g->b, g->b_lo, g->b};
+  for (int s = 0; s < p.nseg; ++s) {
+    int rc = make_operand_map(&p.tma_a[s], as[s], tf32, p.a_mn, g->m, g->k, g->lda, g->a_bstride,
+                              p.a_batched ? g->batch : 1, BM);
+    if (rc) return rc;
+    rc = make_operand_map(&p.tma_b[s], bs[s], tf32, p.b_mn, g->n, g->k, g->ldb, g->b_bstride,
+                          p.b_batched ? g->batch : 1, bn);
+    if (rc) return rc;
+  }
+
+  p.epi = epi;
+  p.alpha = g->alpha;
+  p.d = g->d; p.ldd = g->ldd; p.d_bs = g->d_bstride; p.d_bf16 = g->d_type == JG_BF16;
+  p.d2 = g->d2; p.ldd2 = g->ldd2; p.d2_bs = g->d2_bstride; p.d2_bf16 = g->d2_type == JG_BF16;
+  p.bias = g->bias; p.bias_bs = g->bias_bstride;
+  p.resid = g->resid; p.ldr = g->ldr; p.r_bs = g->r_bstride;
+  p.pre = g->pre; p.ldp = g->ldp; p.p_bs = g->p_bstride; p.pre_bf16 = g->pre_type == JG_BF16;
+  p.stats = g->stats; p.stats_bs = g->stats_bstride;
+
+  if (tf32) {
+    if (bn == 256) return launch<256, true>(p, stream);
+    if (bn == 128) return launch<128, true>(p, stream);
+    return launch<64, true>(p, stream);
+  }
+  if (bn == 256) return launch<256, false>(p, stream);
+  if (bn == 128) return launch<128, false>(p, stream);
+  return launch<64, false>(p, stream);
+}

@@ -1,0 +1,622 @@
+// jg_rowwise.cu — HBM-bound kernels of the WeatherMixer step: layer-norm phases, bias-grad
+// reductions, patch permutes, the fused blend + lat-weighted-MSE tail, Adam, casts.
+// All are coalesced along the contiguous (last) axis, vectorised to 16-byte accesses where
+// the row length allows, warp-reduced, and grid-sized in multiples of the SM count.
+#include "jg_common.cuh"
+
+namespace {
+
+using jgd::warp_sum;
+
+int grid_for(int64_t work_items, int per_block) {
+  int64_t b = (work_items + per_block - 1) / per_block;
+  const int64_t cap = static_cast<int64_t>(jg::num_sms()) * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<int>(b);
+}
+
+// ---------------------------------------------------------------- casts / splits / gelu
+__global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+// 2-D split (optionally transposing) into K-major hi / lo operands for the 3xTF32 GEMM.
+// in : x[b][r][c] (row stride ldx, batch stride xbs); out: [b][transpose ? c : r][ldo] zero-padded.
+__global__ void split_tf32_2d_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                                     int64_t xbs, bool transpose, float* __restrict__ hi, float* __restrict__ lo,
+                                     int64_t ldo) {
+  __shared__ float tile[32][33];
+  const int64_t b = blockIdx.z;
+  const int64_t out_rows = transpose ? cols : rows;
+  const int64_t out_cols = transpose ? rows : cols;
+  const int64_t obs = out_rows * ldo;
+  const float* xb = x + b * xbs;
+  if (!transpose) {
+    const int64_t r = blockIdx.y * 32 + threadIdx.y;
+    for (int64_t rr = r; rr < blockIdx.y * 32 + 32 && rr < rows; rr += 8) {
+      const int64_t c = blockIdx.x * 32 + threadIdx.x;
+      if (c < ldo) {
+        const float v = c < cols ? xb[rr * ldx + c] : 0.f;
+        const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        hi[b * obs + rr * ldo + c] = h;
+        lo[b * obs + rr * ldo + c] = v - h;
+      }
+    }
+    return;
+  }
+  // transpose: read a 32x32 tile of x (rows r0.., cols c0..), write it to out rows c0.., cols r0..
+  const int64_t r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? xb[r * ldx + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t orow = c0 + i, ocol = r0 + threadIdx.x;
+    if (orow < out_rows && ocol < ldo) {
+      const float v = tile[threadIdx.x][i];
+      const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      hi[b * obs + orow * ldo + ocol] = h;
+      lo[b * obs + orow * ldo + ocol] = v - h;
+    }
+  }
+  (void)out_cols;
+}
+
+__global__ void cast_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
+__global__ void gelu_fwd_kernel(const void* __restrict__ x, void* __restrict__ y, bool bf16, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    jgd::store1(y, i, bf16, jgd::gelu_f(jgd::load1(x, i, bf16)));
+}
+
+__global__ void gelu_bwd_kernel(const void* __restrict__ x, const void* __restrict__ g, void* __restrict__ dx,
+                                bool bf16, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    jgd::store1(dx, i, bf16, jgd::load1(g, i, bf16) * jgd::gelu_grad_f(jgd::load1(x, i, bf16)));
+}
+
+// ---------------------------------------------------------------- layer norm
+// Warp per row. The moment formula is the reference's one-pass E[x^2] - mean^2
+// (tensor.py:87-94, model.py:234-237) so sharded partial moments compose exactly.
+__global__ void ln_moments_kernel(const float* __restrict__ x, float* __restrict__ stats, int64_t rows,
+                                  int64_t cols, int64_t ldx) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const bool vec = (cols % 4 == 0) && (ldx % 4 == 0);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const float* xr = x + r * ldx;
+    float s = 0.f, ss = 0.f;
+    if (vec) {
+      for (int64_t c = lane * 4; c < cols; c += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + c);
+        s += v.x + v.y + v.z + v.w;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+    } else {
+      for (int64_t c = lane; c < cols; c += 32) {
+        const float v = xr[c];
+        s += v;
+        ss += v * v;
+      }
+    }
+    s = warp_sum(s);
+    ss = warp_sum(ss);
+    if (lane == 0) {
+      atomicAdd(stats + 2 * r, s);
+      atomicAdd(stats + 2 * r + 1, ss);
+    }
+  }
+}
+
+__global__ void ln_apply_kernel(const float* __restrict__ x, const float* __restrict__ stats,
+                                const float* __restrict__ gamma, const float* __restrict__ beta, void* __restrict__ y,
+                                bool y_bf16, float* __restrict__ mean_rstd, int64_t rows, int64_t cols,
+                                float inv_ctotal, float eps) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const bool vec = (cols % 8 == 0);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const float mean = stats[2 * r] * inv_ctotal;
+    const float var = stats[2 * r + 1] * inv_ctotal - mean * mean;
+    const float rstd = 1.0f / sqrtf(var + eps);
+    if (lane == 0 && mean_rstd) {
+      mean_rstd[2 * r] = mean;
+      mean_rstd[2 * r + 1] = rstd;
+    }
+    const float* xr = x + r * cols;
+    const int64_t yo = r * cols;
+    if (vec) {
+      for (int64_t c = lane * 8; c < cols; c += 256) {
+        float v[8], gm[8], bt[8];
+        jgd::load8(xr, c, false, v);
+        jgd::load8(gamma, c, false, gm);
+        jgd::load8(beta, c, false, bt);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = gm[j] * ((v[j] - mean) * rstd) + bt[j];
+        jgd::store8(y, yo + c, y_bf16, v);
+      }
+    } else {
+      for (int64_t c = lane; c < cols; c += 32)
+        jgd::store1(y, yo + c, y_bf16, gamma[c] * ((xr[c] - mean) * rstd) + beta[c]);
+    }
+  }
+}
+
+__global__ void ln_bwd_moments_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                      const float* __restrict__ gamma, const float* __restrict__ mean_rstd,
+                                      float* __restrict__ bstats, int64_t rows, int64_t cols) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const bool vec = (cols % 8 == 0);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const float mean = mean_rstd[2 * r], rstd = mean_rstd[2 * r + 1];
+    const float* xr = x + r * cols;
+    const float* gr = g + r * cols;
+    float sh = 0.f, shx = 0.f;
+    if (vec) {
+      for (int64_t c = lane * 8; c < cols; c += 256) {
+        float xv[8], gv[8], gm[8];
+        jgd::load8(xr, c, false, xv);
+        jgd::load8(gr, c, false, gv);
+        jgd::load8(gamma, c, false, gm);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float h = gv[j] * gm[j];
+          sh += h;
+          shx += h * ((xv[j] - mean) * rstd);
+        }
+      }
+    } else {
+      for (int64_t c = lane; c < cols; c += 32) {
+        const float h = gr[c] * gamma[c];
+        sh += h;
+        shx += h * ((xr[c] - mean) * rstd);
+      }
+    }
+    sh = warp_sum(sh);
+    shx = warp_sum(shx);
+    if (lane == 0) {
+      atomicAdd(bstats + 2 * r, sh);
+      atomicAdd(bstats + 2 * r + 1, shx);
+    }
+  }
+}
+
+// 2-D tiled: block = 256 threads over 4*256 = 1024 columns, ROWS_PER_BLOCK rows.
+// Column partials of dgamma / dbeta stay in registers; one atomic per column per block.
+constexpr int LNB_ROWS = 64;
+__global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                    const float* __restrict__ gamma, const float* __restrict__ mean_rstd,
+                                    const float* __restrict__ bstats, const float* __restrict__ resid,
+                                    float* __restrict__ out, __nv_bfloat16* __restrict__ out_bf16,
+                                    float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows, int64_t cols,
+                                    float inv_ctotal) {
+  const int64_t c0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
+  const int64_t r0 = blockIdx.y * (int64_t)LNB_ROWS;
+  if (c0 >= cols) return;
+  const int64_t r1 = r0 + LNB_ROWS < rows ? r0 + LNB_ROWS : rows;
+  const int nc = cols - c0 >= 4 ? 4 : static_cast<int>(cols - c0);
+  float gm[4], dg[4] = {0, 0, 0, 0}, db[4] = {0, 0, 0, 0};
+  for (int j = 0; j < 4; ++j) gm[j] = j < nc ? gamma[c0 + j] : 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float mean = mean_rstd[2 * r], rstd = mean_rstd[2 * r + 1];
+    const float msh = bstats[2 * r] * inv_ctotal, mshx = bstats[2 * r + 1] * inv_ctotal;
+    const int64_t o = r * cols + c0;
+    float xv[4], gv[4], rv[4] = {0, 0, 0, 0}, ov[4];
+    if (nc == 4 && (cols % 4 == 0)) {
+      const float4 a = *reinterpret_cast<const float4*>(x + o);
+      const float4 b = *reinterpret_cast<const float4*>(g + o);
+      xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+      gv[0] = b.x; gv[1] = b.y; gv[2] = b.z; gv[3] = b.w;
+      if (resid) {
+        const float4 c = *reinterpret_cast<const float4*>(resid + o);
+        rv[0] = c.x; rv[1] = c.y; rv[2] = c.z; rv[3] = c.w;
+      }
+    } else {
+      for (int j = 0; j < 4; ++j) {
+        xv[j] = j < nc ? x[o + j] : 0.f;
+        gv[j] = j < nc ? g[o + j] : 0.f;
+        rv[j] = (resid && j < nc) ? resid[o + j] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float xh = (xv[j] - mean) * rstd;
+      const float h = gv[j] * gm[j];
+      ov[j] = rv[j] + rstd * (h - msh - xh * mshx);
+      dg[j] += gv[j] * xh;
+      db[j] += gv[j];
+    }
+    if (nc == 4 && (cols % 4 == 0)) {
+      *reinterpret_cast<float4*>(out + o) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+      if (out_bf16) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(ov[0], ov[1]), hi = __floats2bfloat162_rn(ov[2], ov[3]);
+        uint2 raw;
+        raw.x = *reinterpret_cast<uint32_t*>(&lo);
+        raw.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(out_bf16 + o) = raw;
+      }
+    } else {
+      for (int j = 0; j < nc; ++j) {
+        out[o + j] = ov[j];
+        if (out_bf16) out_bf16[o + j] = __float2bfloat16_rn(ov[j]);
+      }
+    }
+  }
+  for (int j = 0; j < nc; ++j) {
+    if (dgamma) atomicAdd(dgamma + c0 + j, dg[j]);
+    if (dbeta) atomicAdd(dbeta + c0 + j, db[j]);
+  }
+}
+
+// ---------------------------------------------------------------- bias-grad reductions
+constexpr int CS_ROWS = 128;
+__global__ void colsum_kernel(const void* __restrict__ x, bool bf16, float* __restrict__ out, int64_t rows,
+                              int64_t cols, int64_t ldx) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int64_t r0 = blockIdx.y * (int64_t)CS_ROWS;
+  const int64_t r1 = r0 + CS_ROWS < rows ? r0 + CS_ROWS : rows;
+  float s = 0.f;
+  for (int64_t r = r0; r < r1; ++r) s += jgd::load1(x, r * ldx + c, bf16);
+  atomicAdd(out + c, s);
+}
+
+__global__ void rowsum_kernel(const void* __restrict__ x, bool bf16, float* __restrict__ out, int64_t rows,
+                              int64_t cols, int64_t ldx) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    float s = 0.f;
+    for (int64_t c = lane; c < cols; c += 32) s += jgd::load1(x, r * ldx + c, bf16);
+    s = warp_sum(s);
+    if (lane == 0) out[r] += s;
+  }
+}
+
+// ---------------------------------------------------------------- patch permutes
+// token t = gi*gw + gj ; feature f = c*pl*pw + i*pw + j ; grid (gi*pl+i, gj*pw+j, c)
+__global__ void patchify_kernel(const float* __restrict__ x, void* __restrict__ tok, bool bf16, int64_t batch,
+                                int64_t lat, int64_t lon, int64_t chans, int64_t pl, int64_t pw) {
+  const int64_t gw = lon / pw, T = (lat / pl) * gw, F = chans * pl * pw;
+  const int64_t n = batch * T * F;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = idx % F;
+    const int64_t t = (idx / F) % T;
+    const int64_t b = idx / (F * T);
+    const int64_t c = f / (pl * pw), i = (f / pw) % pl, j = f % pw;
+    const int64_t gi = t / gw, gj = t % gw;
+    jgd::store1(tok, idx, bf16, x[((b * lat + gi * pl + i) * lon + gj * pw + j) * chans + c]);
+  }
+}
+
+__global__ void unpatchify_kernel(const float* __restrict__ tok, float* __restrict__ x, int64_t batch, int64_t lat,
+                                  int64_t lon, int64_t chans, int64_t pl, int64_t pw) {
+  const int64_t gw = lon / pw, T = (lat / pl) * gw, F = chans * pl * pw;
+  const int64_t n = batch * lat * lon * chans;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx % chans;
+    const int64_t xo = (idx / chans) % lon;
+    const int64_t ya = (idx / (chans * lon)) % lat;
+    const int64_t b = idx / (chans * lon * lat);
+    const int64_t t = (ya / pl) * gw + xo / pw;
+    const int64_t f = c * pl * pw + (ya % pl) * pw + (xo % pw);
+    x[idx] = tok[(b * T + t) * F + f];
+  }
+}
+
+// ---------------------------------------------------------------- blend + loss
+// One thread per grid element (coalesced over [B,lat,lon,C]); gathers / scatters the token
+// layout. Per-channel blend gradient and the loss are block-reduced in shared memory.
+constexpr int MAX_CH = 1024;
+__global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float* __restrict__ x,
+                                  const float* __restrict__ target, const float* __restrict__ blend_w,
+                                  const float* __restrict__ lat_w, const float* __restrict__ var_w,
+                                  const float* __restrict__ g_ext, float* __restrict__ out, float* __restrict__ loss_sum,
+                                  float* __restrict__ g_blend, float* __restrict__ g_dec_f32,
+                                  __nv_bfloat16* __restrict__ g_dec_bf16, int64_t batch, int64_t lat, int64_t lon,
+                                  int64_t chans, int64_t pl, int64_t pw, float inv_count, float loss_scale) {
+  __shared__ float s_gb[MAX_CH];
+  __shared__ float s_loss[32];
+  for (int c = threadIdx.x; c < chans; c += blockDim.x) s_gb[c] = 0.f;
+  __syncthreads();
+  const int64_t gw = lon / pw, T = (lat / pl) * gw, F = chans * pl * pw;
+  const int64_t n = batch * lat * lon * chans;
+  float lsum = 0.f;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx % chans;
+    const int64_t xo = (idx / chans) % lon;
+    const int64_t ya = (idx / (chans * lon)) % lat;
+    const int64_t b = idx / (chans * lon * lat);
+    const int64_t t = (ya / pl) * gw + xo / pw;
+    const int64_t f = c * pl * pw + (ya % pl) * pw + (xo % pw);
+    const int64_t to = (b * T + t) * F + f;
+    const float dec = dec_tok[to];
+    const float xv = x[idx];
+    const float w = blend_w[c];
+    const float o = w * dec + (1.0f - w) * xv;
+    if (out) out[idx] = o;
+    float g;
+    if (g_ext) {
+      g = g_ext[idx];
+    } else {
+      const float wt = lat_w[ya] * var_w[c];
+      const float e = o - target[idx];
+      lsum += wt * e * e;
+      g = 2.0f * wt * e * inv_count * loss_scale;
+    }
+    atomicAdd(&s_gb[c], g * (dec - xv));
+    const float gd = g * w;
+    if (g_dec_f32) g_dec_f32[to] = gd;
+    if (g_dec_bf16) g_dec_bf16[to] = __float2bfloat16_rn(gd);
+  }
+  lsum = warp_sum(lsum);
+  if ((threadIdx.x & 31) == 0) s_loss[threadIdx.x >> 5] = lsum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? s_loss[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0 && loss_sum && !g_ext) atomicAdd(loss_sum, v * inv_count);
+  }
+  for (int c = threadIdx.x; c < chans; c += blockDim.x)
+    if (g_blend) atomicAdd(g_blend + c, s_gb[c]);
+}
+
+// ---------------------------------------------------------------- Adam
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, __nv_bfloat16* __restrict__ pb, int64_t n, float lr, float b1,
+                            float b2, float eps, const int32_t* __restrict__ step, const float* __restrict__ gscale) {
+  const int t = *step;
+  const float bc1 = 1.0f / (1.0f - powf(b1, (float)t));
+  const float bc2 = 1.0f / (1.0f - powf(b2, (float)t));
+  const float s = gscale ? *gscale : 1.0f;
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float* pa = &pp.x; const float* ga = &gg.x; float* ma = &mm.x; float* va = &vv.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float gj = ga[j] * s;
+      ma[j] = b1 * ma[j] + (1.0f - b1) * gj;
+      va[j] = b2 * va[j] + (1.0f - b2) * gj * gj;
+      pa[j] -= lr * (ma[j] * bc1) / (sqrtf(va[j] * bc2) + eps);
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (pb) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y), hi = __floats2bfloat162_rn(pp.z, pp.w);
+      uint2 raw;
+      raw.x = *reinterpret_cast<uint32_t*>(&lo);
+      raw.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(pb)[i] = raw;
+    }
+  }
+  // scalar tail
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gj = g[i] * s;
+    m[i] = b1 * m[i] + (1.0f - b1) * gj;
+    v[i] = b2 * v[i] + (1.0f - b2) * gj * gj;
+    p[i] -= lr * (m[i] * bc1) / (sqrtf(v[i] * bc2) + eps);
+    if (pb) pb[i] = __float2bfloat16_rn(p[i]);
+  }
+}
+
+__global__ void step_inc_kernel(int32_t* counter) { *counter += 1; }
+
+__global__ void sqnorm_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+  __shared__ float part[32];
+  float s = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    s += v * v;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) atomicAdd(out, v);
+  }
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int jg_split_tf32(const float* x, float* hi, float* lo, int64_t n, void* stream) {
+  JG_SHAPE_CHECK(n >= 0, "jg_split_tf32: negative size");
+  if (n == 0) return JG_OK;
+  split_tf32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, hi, lo, n);
+  JG_LAUNCH_CHECK("split_tf32");
+  return JG_OK;
+}
+
+int jg_split_tf32_2d(const float* x, int64_t rows, int64_t cols, int64_t ldx, int64_t batch, int64_t x_bstride,
+                     int32_t transpose, float* hi, float* lo, int64_t ldo, void* stream) {
+  JG_SHAPE_CHECK(rows > 0 && cols > 0 && batch > 0 && ldx >= cols, "jg_split_tf32_2d: bad shape");
+  JG_SHAPE_CHECK(ldo >= (transpose ? rows : cols), "jg_split_tf32_2d: ldo too small");
+  dim3 block(32, 8);
+  dim3 grid;
+  if (transpose)
+    grid = dim3((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32), (unsigned)batch);
+  else
+    grid = dim3((unsigned)((ldo + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
+  split_tf32_2d_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(x, rows, cols, ldx, x_bstride, transpose != 0, hi,
+                                                                 lo, ldo);
+  JG_LAUNCH_CHECK("split_tf32_2d");
+  return JG_OK;
+}
+
+int jg_cast_bf16(const float* x, void* y, int64_t n, void* stream) {
+  if (n == 0) return JG_OK;
+  cast_bf16_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)y, n);
+  JG_LAUNCH_CHECK("cast_bf16");
+  return JG_OK;
+}
+
+int jg_gelu_fwd(const void* x, void* y, int32_t dtype, int64_t n, void* stream) {
+  JG_SHAPE_CHECK(dtype == JG_F32 || dtype == JG_BF16, "jg_gelu_fwd: bad dtype %d", dtype);
+  if (n == 0) return JG_OK;
+  gelu_fwd_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, y, dtype == JG_BF16, n);
+  JG_LAUNCH_CHECK("gelu_fwd");
+  return JG_OK;
+}
+
+int jg_gelu_bwd(const void* x, const void* g, void* dx, int32_t dtype, int64_t n, void* stream) {
+  JG_SHAPE_CHECK(dtype == JG_F32 || dtype == JG_BF16, "jg_gelu_bwd: bad dtype %d", dtype);
+  if (n == 0) return JG_OK;
+  gelu_bwd_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, g, dx, dtype == JG_BF16, n);
+  JG_LAUNCH_CHECK("gelu_bwd");
+  return JG_OK;
+}
+
+int jg_ln_moments(const float* x, float* stats, int64_t rows, int64_t cols, int64_t ldx, void* stream) {
+  JG_SHAPE_CHECK(rows >= 0 && cols > 0 && ldx >= cols, "jg_ln_moments: bad shape");
+  if (rows == 0) return JG_OK;
+  ln_moments_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(x, stats, rows, cols, ldx);
+  JG_LAUNCH_CHECK("ln_moments");
+  return JG_OK;
+}
+
+int jg_ln_apply(const float* x, const float* stats, const float* gamma, const float* beta, void* y, int32_t y_type,
+                float* mean_rstd, int64_t rows, int64_t cols, int64_t c_total, float eps, void* stream) {
+  JG_SHAPE_CHECK(eps > 0.f, "layer_norm eps must be > 0, got %g", (double)eps);
+  JG_SHAPE_CHECK(rows >= 0 && cols > 0 && c_total >= cols, "jg_ln_apply: bad shape");
+  JG_SHAPE_CHECK(al16(x) && al16(y) && al16(gamma) && al16(beta), "jg_ln_apply: pointers must be 16B aligned");
+  if (rows == 0) return JG_OK;
+  ln_apply_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(x, stats, gamma, beta, y, y_type == JG_BF16,
+                                                                      mean_rstd, rows, cols, 1.0f / (float)c_total, eps);
+  JG_LAUNCH_CHECK("ln_apply");
+  return JG_OK;
+}
+
+int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const float* mean_rstd, float* bstats,
+                      int64_t rows, int64_t cols, void* stream) {
+  JG_SHAPE_CHECK(rows >= 0 && cols > 0, "jg_ln_bwd_moments: bad shape");
+  JG_SHAPE_CHECK(al16(x) && al16(g) && al16(gamma), "jg_ln_bwd_moments: pointers must be 16B aligned");
+  if (rows == 0) return JG_OK;
+  ln_bwd_moments_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(x, g, gamma, mean_rstd, bstats, rows, cols);
+  JG_LAUNCH_CHECK("ln_bwd_moments");
+  return JG_OK;
+}
+
+int jg_ln_bwd_apply(const float* x, const float* g, const float* gamma, const float* mean_rstd, const float* bstats,
+                    const float* resid, float* out, void* out_bf16, float* dgamma, float* dbeta, float* rowsum_out,
+                    int64_t rows, int64_t cols, int64_t c_total, void* stream) {
+  JG_SHAPE_CHECK(rows >= 0 && cols > 0 && c_total >= cols, "jg_ln_bwd_apply: bad shape");
+  JG_SHAPE_CHECK(al16(x) && al16(g) && al16(out) && (!resid || al16(resid)), "jg_ln_bwd_apply: pointers must be 16B aligned");
+  if (rows == 0) return JG_OK;
+  dim3 grid((unsigned)((cols + 1023) / 1024), (unsigned)((rows + LNB_ROWS - 1) / LNB_ROWS));
+  ln_bwd_apply_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, g, gamma, mean_rstd, bstats, resid, out,
+                                                               (__nv_bfloat16*)out_bf16, dgamma, dbeta, rows, cols,
+                                                               1.0f / (float)c_total);
+  JG_LAUNCH_CHECK("ln_bwd_apply");
+  if (rowsum_out) {
+    rowsum_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(out, false, rowsum_out, rows, cols, cols);
+    JG_LAUNCH_CHECK("rowsum");
+  }
+  return JG_OK;
+}
+
+int jg_colsum(const void* x, int32_t x_type, float* out, int64_t rows, int64_t cols, int64_t ldx, void* stream) {
+  JG_SHAPE_CHECK(rows >= 0 && cols > 0 && ldx >= cols, "jg_colsum: bad shape");
+  if (rows == 0) return JG_OK;
+  dim3 grid((unsigned)((cols + 255) / 256), (unsigned)((rows + CS_ROWS - 1) / CS_ROWS));
+  colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, x_type == JG_BF16, out, rows, cols, ldx);
+  JG_LAUNCH_CHECK("colsum");
+  return JG_OK;
+}
+
+int jg_rowsum(const void* x, int32_t x_type, float* out, int64_t rows, int64_t cols, int64_t ldx, void* stream) {
+  JG_SHAPE_CHECK(rows >= 0 && cols > 0 && ldx >= cols, "jg_rowsum: bad shape");
+  if (rows == 0) return JG_OK;
+  rowsum_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(x, x_type == JG_BF16, out, rows, cols, ldx);
+  JG_LAUNCH_CHECK("rowsum");
+  return JG_OK;
+}
+
+int jg_patchify(const float* x, void* tokens, int32_t t_type, int64_t batch, int64_t lat, int64_t lon, int64_t chans,
+                int64_t p_lat, int64_t p_lon, void* stream) {
+  JG_SHAPE_CHECK(p_lat > 0 && p_lon > 0 && lat % p_lat == 0 && lon % p_lon == 0,
+                 "grid %lldx%lld not divisible by patch %lldx%lld", (long long)lat, (long long)lon, (long long)p_lat,
+                 (long long)p_lon);
+  const int64_t n = batch * lat * lon * chans;
+  if (n == 0) return JG_OK;
+  patchify_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, tokens, t_type == JG_BF16, batch, lat, lon,
+                                                                     chans, p_lat, p_lon);
+  JG_LAUNCH_CHECK("patchify");
+  return JG_OK;
+}
+
+int jg_unpatchify(const float* tokens, float* x, int64_t batch, int64_t lat, int64_t lon, int64_t chans, int64_t p_lat,
+                  int64_t p_lon, void* stream) {
+  JG_SHAPE_CHECK(p_lat > 0 && p_lon > 0 && lat % p_lat == 0 && lon % p_lon == 0,
+                 "token tensor does not fit grid %lldx%lld", (long long)lat, (long long)lon);
+  const int64_t n = batch * lat * lon * chans;
+  if (n == 0) return JG_OK;
+  unpatchify_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(tokens, x, batch, lat, lon, chans, p_lat, p_lon);
+  JG_LAUNCH_CHECK("unpatchify");
+  return JG_OK;
+}
+
+int jg_blend_loss(const float* dec_tok, const float* x, const float* target, const float* blend_w, const float* lat_w,
+                  const float* var_w, const float* g_out_ext, float* out, float* loss_sum, float* g_blend,
+                  float* g_dec_f32, void* g_dec_bf16, int64_t batch, int64_t lat, int64_t lon, int64_t chans,
+                  int64_t p_lat, int64_t p_lon, float inv_count, float loss_scale, void* stream) {
+  JG_SHAPE_CHECK(chans <= MAX_CH, "jg_blend_loss: at most %d channels", MAX_CH);
+  JG_SHAPE_CHECK(lat % p_lat == 0 && lon % p_lon == 0, "jg_blend_loss: grid not divisible by patch");
+  JG_SHAPE_CHECK(g_out_ext || (target && lat_w && var_w), "jg_blend_loss: need target + weights or g_out_ext");
+  const int64_t n = batch * lat * lon * chans;
+  if (n == 0) return JG_OK;
+  blend_loss_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      dec_tok, x, target, blend_w, lat_w, var_w, g_out_ext, out, loss_sum, g_blend, g_dec_f32,
+      (__nv_bfloat16*)g_dec_bf16, batch, lat, lon, chans, p_lat, p_lon, inv_count, loss_scale);
+  JG_LAUNCH_CHECK("blend_loss");
+  return JG_OK;
+}
+
+int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, float lr, float beta1, float beta2,
+            float eps, const int32_t* step_dev, const float* grad_scale_dev, void* stream) {
+  JG_SHAPE_CHECK(n >= 0 && step_dev, "jg_adam: bad arguments");
+  JG_SHAPE_CHECK(al16(p) && al16(g) && al16(m) && al16(v) && (!p_bf16 || (reinterpret_cast<uintptr_t>(p_bf16) & 7u) == 0),
+                 "jg_adam: buffers must be 16B aligned");
+  if (n == 0) return JG_OK;
+  adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+      p, g, m, v, (__nv_bfloat16*)p_bf16, n, lr, beta1, beta2, eps, step_dev, grad_scale_dev);
+  JG_LAUNCH_CHECK("adam");
+  return JG_OK;
+}
+
+int jg_step_increment(int32_t* counter, void* stream) {
+  step_inc_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(counter);
+  JG_LAUNCH_CHECK("step_inc");
+  return JG_OK;
+}
+
+int jg_sqnorm(const float* x, int64_t n, float* out, void* stream) {
+  if (n == 0) return JG_OK;
+  sqnorm_kernel<<<grid_for(n, 1024), 256, 0, (cudaStream_t)stream>>>(x, n, out);
+  JG_LAUNCH_CHECK("sqnorm");
+  return JG_OK;
+}
+
+}  // extern "C"

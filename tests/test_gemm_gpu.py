@@ -1,0 +1,133 @@
+"""tcgen05 GEMM parity against an fp64 reference of the same contraction (tensor.py:59-72 semantics)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(a, b, mode):
+    a64, b64 = a.double().cpu(), b.double().cpu()
+    if mode == "NN":
+        return a64 @ b64
+    if mode == "NT":
+        return a64 @ b64.transpose(-1, -2)
+    return a64.transpose(-1, -2) @ b64
+
+
+SHAPES = [(128, 128, 64), (64, 64, 128), (200, 300, 100), (384, 520, 272), (1000, 1030, 333), (4320 // 4, 4480 // 4, 1024)]
+
+
+@pytest.mark.parametrize("mode", ["NN", "NT", "TN"])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_matmul_modes(cuda, mode, shape, dtype):
+    from paper_2507_05753_b200 import tensor as T
+    m, n, k = shape
+    g = torch.Generator(device="cpu").manual_seed(m * 7 + n * 3 + k)
+    if mode == "NN":
+        a, b = torch.randn(m, k, generator=g), torch.randn(k, n, generator=g)
+    elif mode == "NT":
+        a, b = torch.randn(m, k, generator=g), torch.randn(n, k, generator=g)
+    else:
+        a, b = torch.randn(k, m, generator=g), torch.randn(k, n, generator=g)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    a_d, b_d = a.to(cuda, tdt), b.to(cuda, tdt)
+    out = T.matmul(a_d, b_d, mode)
+    torch.cuda.synchronize()
+    ref = _ref(a_d.float(), b_d.float(), mode)  # exact product of the (rounded) operands
+    err = rel_err(out.float().cpu().numpy(), ref.numpy())
+    tol = 5e-5 if dtype == "f32" else 1e-2
+    assert err < tol, (mode, shape, dtype, err)
+
+
+@pytest.mark.parametrize("mode", ["NN", "NT", "TN"])
+def test_matmul_batched_broadcast(cuda, mode):
+    from paper_2507_05753_b200 import tensor as T
+    g = torch.Generator(device="cpu").manual_seed(5)
+    m, n, k = 136, 200, 96
+    if mode == "NN":
+        a, b = torch.randn(3, m, k, generator=g), torch.randn(k, n, generator=g)
+    elif mode == "NT":
+        a, b = torch.randn(3, m, k, generator=g), torch.randn(n, k, generator=g)
+    else:
+        a, b = torch.randn(3, k, m, generator=g), torch.randn(k, n, generator=g)
+    out = T.matmul(a.cuda(), b.cuda(), mode)
+    ref = _ref(a, b, mode)
+    assert out.shape == ref.shape
+    assert rel_err(out.cpu().numpy(), ref.numpy()) < 2e-5
+
+
+def test_fixed_nt_example(cuda):
+    # reference test_tensor.py:23-28
+    from paper_2507_05753_b200 import tensor as T
+    a = torch.tensor([[1.0, 2.0], [3.0, 4.0]], device=cuda)
+    b = torch.tensor([[5.0, 6.0], [7.0, 8.0]], device=cuda)
+    out = T.matmul(a, b, "NT")
+    assert out.cpu().tolist() == [[17.0, 23.0], [39.0, 53.0]]
+    outb = T.matmul(a.bfloat16(), b.bfloat16(), "NT")
+    assert outb.float().cpu().tolist() == [[17.0, 23.0], [39.0, 53.0]]
+
+
+def test_epilogue_fusions(cuda):
+    """bias / residual / GELU fwd / GELU bwd / accumulate / stats epilogues vs torch fp64."""
+    from paper_2507_05753_b200 import tensor as T, _lib
+    g = torch.Generator(device="cpu").manual_seed(11)
+    m, n, k = 300, 264, 200
+    a = torch.randn(m, k, generator=g).cuda()
+    w = torch.randn(n, k, generator=g).cuda()
+    bias = torch.randn(n, generator=g).cuda()
+    rbias = torch.randn(m, generator=g).cuda()
+    resid = torch.randn(m, n, generator=g).cuda()
+    pre = torch.randn(m, n, generator=g).cuda()
+    acc = (a.double() @ w.double().T)
+    # bias col + resid + stats + bf16 copy
+    d = torch.empty(m, n, device=cuda)
+    d2 = torch.empty(m, n, device=cuda, dtype=torch.bfloat16)
+    st = torch.zeros(m, 2, device=cuda)
+    T.gemm_into(d, a, w, _lib.JG_KMAJOR, _lib.JG_KMAJOR, m, n, k,
+                epi=_lib.EPI_BIAS_COL | _lib.EPI_RESID | _lib.EPI_STATS | _lib.EPI_COPY_D2,
+                bias=bias, resid=resid, stats=st, d2=d2)
+    ref = acc + bias.double() + resid.double()
+    assert rel_err(d.cpu(), ref.cpu()) < 2e-5
+    assert rel_err(d2.float().cpu(), ref.cpu()) < 1e-2
+    assert rel_err(st[:, 0].cpu(), ref.sum(1).cpu()) < 1e-5
+    assert rel_err(st[:, 1].cpu(), (ref * ref).sum(1).cpu()) < 1e-5
+    # row bias + gelu fwd
+    d = torch.empty(m, n, device=cuda)
+    d2 = torch.empty(m, n, device=cuda)
+    T.gemm_into(d, a, w, _lib.JG_KMAJOR, _lib.JG_KMAJOR, m, n, k, epi=_lib.EPI_BIAS_ROW | _lib.EPI_GELU_FWD,
+                bias=rbias, d2=d2)
+    ref = acc + rbias.double()[:, None]
+    assert rel_err(d.cpu(), ref.cpu()) < 2e-5
+    gref = ref * 0.5 * (1 + torch.erf(ref / np.sqrt(2)))
+    assert rel_err(d2.cpu(), gref.cpu()) < 2e-5
+    # gelu bwd
+    d = torch.empty(m, n, device=cuda)
+    T.gemm_into(d, a, w, _lib.JG_KMAJOR, _lib.JG_KMAJOR, m, n, k, epi=_lib.EPI_GELU_BWD, pre=pre)
+    p64 = pre.double()
+    dg = 0.5 * (1 + torch.erf(p64 / np.sqrt(2))) + p64 * torch.exp(-0.5 * p64 * p64) / np.sqrt(2 * np.pi)
+    assert rel_err(d.cpu(), (acc * dg).cpu()) < 2e-5
+    # accumulate
+    d = resid.clone()
+    T.gemm_into(d, a, w, _lib.JG_KMAJOR, _lib.JG_KMAJOR, m, n, k, epi=_lib.EPI_ACCUM)
+    assert rel_err(d.cpu(), (acc + resid.double()).cpu()) < 2e-5
+
+
+def test_reduce_batch(cuda):
+    """sum_b A[b]^T B[b] with the batch folded into the K loop (weight-gradient form)."""
+    from paper_2507_05753_b200 import tensor as T, _lib
+    g = torch.Generator(device="cpu").manual_seed(3)
+    bsz, t, e, dt = 3, 160, 136, 200
+    u = torch.randn(bsz, t, e, generator=g).cuda()
+    gh = torch.randn(bsz, e, dt, generator=g).cuda()
+    # dW1[t, j] = sum_b sum_e u[b,t,e] gh[b,e,j] : A = u K-major (K = e), B = gh MN-major
+    out = torch.zeros(t, dt, device=cuda)
+    T.gemm_into(out, u, gh, _lib.JG_KMAJOR, _lib.JG_MNMAJOR, t, dt, e, bsz, t * e, e * dt,
+                reduce_batch=True, epi=_lib.EPI_ACCUM)
+    ref = torch.einsum("bte,bej->tj", u.double(), gh.double())
+    assert rel_err(out.cpu(), ref.cpu()) < 2e-5
