@@ -150,7 +150,8 @@ int jg_unpatchify(const float* tokens, float* x, int64_t batch, int64_t lat, int
  *   g_dec_tok = patchify(g_out * w)  written as fp32 and/or bf16                  (model.py:438-439)
  * out / g_dec_f32 / g_dec_bf16 may be NULL. loss_sum is one fp32 scalar (pre-zeroed).
  * g_out_ext (optional, [B,lat,lon,C] fp32): when non-NULL it REPLACES the MSE gradient
- * (the reference's model.backward(g_out) entry point, model.py:428).
+ * (the reference's model.backward(g_out) entry point, model.py:428). With neither target nor
+ * g_out_ext only the forward blend (out) is computed (model.forward, model.py:420-426).
  */
 int jg_blend_loss(const float* dec_tok, const float* x, const float* target, const float* blend_w,
                   const float* lat_w, const float* var_w, const float* g_out_ext,

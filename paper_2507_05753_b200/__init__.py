@@ -1,0 +1,20 @@
+"""B200-native (sm_100a) WeatherMixer training step under Jigsaw parallelism (arXiv 2507.05753).
+
+Drop-in for the reference `jigsaw` package's hot path: same names as its __init__.py
+(ModelConfig, WeatherMixerModel, MpContext, pnt/pnn/ptn, comm_volume, ShardSpec, shard,
+gather, MatmulMode, ProcessGroup), executed by hand-written tcgen05/TMA kernels in
+libjigsaw_sm100.so and NCCL over NVLink.
+"""
+from .comm import Communicator, ProcessGroup
+from .config import ModelConfig
+from .errors import CommError, CommTimeout, ConfigError, ShapeError, WorkerError
+from .model import Layout, WeatherMixerModel
+from .parallel import MpContext, comm_volume, pnn, pnt, ptn
+from .sharding import ShardSpec, gather, shard
+from .tensor import MatmulMode
+
+__all__ = [
+    "Communicator", "CommError", "CommTimeout", "ConfigError", "Layout", "MatmulMode", "ModelConfig",
+    "MpContext", "ProcessGroup", "ShapeError", "ShardSpec", "WeatherMixerModel", "WorkerError",
+    "comm_volume", "gather", "pnn", "pnt", "ptn", "shard",
+]

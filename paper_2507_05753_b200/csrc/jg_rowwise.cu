@@ -347,6 +347,7 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
     const float w = blend_w[c];
     const float o = w * dec + (1.0f - w) * xv;
     if (out) out[idx] = o;
+    if (!g_ext && !target) continue;  // forward only
     float g;
     if (g_ext) {
       g = g_ext[idx];
@@ -369,8 +370,8 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
     v = warp_sum(v);
     if (threadIdx.x == 0 && loss_sum && !g_ext) atomicAdd(loss_sum, v * inv_count);
   }
-  for (int c = threadIdx.x; c < chans; c += blockDim.x)
-    if (g_blend) atomicAdd(g_blend + c, s_gb[c]);
+  if (g_blend && (g_ext || target))
+    for (int c = threadIdx.x; c < chans; c += blockDim.x) atomicAdd(g_blend + c, s_gb[c]);
 }
 
 // ---------------------------------------------------------------- Adam
@@ -584,7 +585,7 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
                   int64_t p_lat, int64_t p_lon, float inv_count, float loss_scale, void* stream) {
   JG_SHAPE_CHECK(chans <= MAX_CH, "jg_blend_loss: at most %d channels", MAX_CH);
   JG_SHAPE_CHECK(lat % p_lat == 0 && lon % p_lon == 0, "jg_blend_loss: grid not divisible by patch");
-  JG_SHAPE_CHECK(g_out_ext || (target && lat_w && var_w), "jg_blend_loss: need target + weights or g_out_ext");
+  JG_SHAPE_CHECK(!target || (lat_w && var_w), "jg_blend_loss: a target needs lat/var weights");
   const int64_t n = batch * lat * lon * chans;
   if (n == 0) return JG_OK;
   blend_loss_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(

@@ -1,0 +1,95 @@
+"""Parameter shards in flat HBM buffers (reference Param, parallel.py:469-493).
+
+Every local parameter shard of a model is a view into a handful of flat device buffers, one
+per role, laid out lr-class by lr-class so the optimiser is one fused kernel per class:
+
+  master fp32  (Param.data)   grad fp32 (Param.grad)   m, v fp32 (Adam moments)
+  op           GEMM-operand copy: bf16 in bf16 mode (written by the Adam kernel), or the
+               master itself in fp32 mode.
+
+Offsets are aligned to 64 elements so every view satisfies the 16-byte TMA / vector-access
+alignment. Zeroing all gradients is one memset (reference zero_grads, model.py:447-449).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+ALIGN = 64
+
+
+@dataclass
+class Param:
+    """One locally stored parameter shard with gradient accumulation (parallel.py:469-493)."""
+
+    name: str
+    data: torch.Tensor
+    lr_class: str = "body"
+    dup_positions: tuple[int, ...] = ()
+    grad: torch.Tensor | None = field(default=None, repr=False)
+    op: torch.Tensor | None = field(default=None, repr=False)  # GEMM operand copy (bf16 or == data)
+
+    @property
+    def dup_factor(self) -> int:
+        return max(1, len(self.dup_positions))
+
+    def zero_grad(self) -> None:
+        if self.grad is None:
+            self.grad = torch.zeros_like(self.data)
+        else:
+            self.grad.zero_()
+
+    def add_grad(self, g: torch.Tensor) -> None:
+        if self.grad is None:
+            self.grad = torch.zeros_like(self.data)
+        self.grad += g
+
+
+class FlatParams:
+    """Owns the flat buffers; hands out Param views in registration order."""
+
+    CLASSES = ("encdec", "body")
+
+    def __init__(self, specs, device, op_dtype: torch.dtype):
+        # specs: list of (name, local_shape, lr_class, dup_positions) in registration order
+        self.specs = list(specs)
+        self.device = device
+        self.op_dtype = op_dtype
+        self.offsets: dict[str, int] = {}
+        self.class_range: dict[str, tuple[int, int]] = {}
+        off = 0
+        for cls in self.CLASSES:
+            start = off
+            for name, shape, lr_class, _ in self.specs:
+                if lr_class != cls:
+                    continue
+                self.offsets[name] = off
+                numel = 1
+                for s in shape:
+                    numel *= s
+                off += -(-numel // ALIGN) * ALIGN
+            self.class_range[cls] = (start, off)
+        self.total = off
+        f32 = dict(dtype=torch.float32, device=device)
+        self.master = torch.zeros(self.total, **f32)
+        self.grad = torch.zeros(self.total, **f32)
+        self.m = torch.zeros(self.total, **f32)
+        self.v = torch.zeros(self.total, **f32)
+        self.op = self.master if op_dtype == torch.float32 else torch.zeros(self.total, dtype=op_dtype, device=device)
+        self.params: dict[str, Param] = {}
+        for name, shape, lr_class, dup in self.specs:
+            o = self.offsets[name]
+            numel = 1
+            for s in shape:
+                numel *= s
+            p = Param(name, self.master[o:o + numel].view(shape), lr_class, tuple(dup))
+            p.grad = self.grad[o:o + numel].view(shape)
+            p.op = self.op[o:o + numel].view(shape)
+            self.params[name] = p
+
+    def zero_grads(self) -> None:
+        self.grad.zero_()
+
+    def numel(self) -> int:
+        return sum(p.data.numel() for p in self.params.values())
