@@ -166,6 +166,47 @@ class SerialModel:
         y, xhat, inv = ops.ln_from_moments(x, s, sq, x.shape[-1], self.p[pre + "gamma"], self.p[pre + "beta"], self.eps)
         return y, (xhat, inv)
 
+    def block_forward(self, i: int, h):
+        """MixerBlock.forward (model.py:268-282) at n = 1."""
+        p, b = self.p, f"block{i}."
+        u, c_ln1 = self._ln(h, b + "ln1.")
+        t1 = ops.matmul(u, p[b + "tok1.w"], "TN") + p[b + "tok1.b"]          # [B, E, K]
+        a = ops.gelu(t1)
+        o = ops.matmul(p[b + "tok2.w"], a, "NT") + p[b + "tok2.b"][:, None]  # [B, T, E]
+        x2 = h + o
+        v, c_ln2 = self._ln(x2, b + "ln2.")
+        cc = ops.matmul(v, p[b + "ch1.w"], "NT") + p[b + "ch1.b"]
+        ca = ops.gelu(cc)
+        z = ops.matmul(ca, p[b + "ch2.w"], "NT") + p[b + "ch2.b"]
+        return x2 + z, (h, c_ln1, u, t1, a, c_ln2, v, cc, ca)
+
+    def block_backward(self, i: int, cache, gh, grads):
+        """MixerBlock.backward (model.py:284-297) at n = 1; accumulates into grads."""
+        p, b, cfg = self.p, f"block{i}.", self.cfg
+        h, c_ln1, u, t1, a, c_ln2, v, cc, ca = cache
+        grads[b + "ch2.w"] += _flat(ops.matmul(gh, ca, "TN"))
+        grads[b + "ch2.b"] += gh.sum(axis=(0, 1))
+        g_c = ops.gelu_backward(cc, ops.matmul(gh, p[b + "ch2.w"], "NN"))
+        grads[b + "ch1.w"] += _flat(ops.matmul(g_c, v, "TN"))
+        grads[b + "ch1.b"] += g_c.sum(axis=(0, 1))
+        g_v = ops.matmul(g_c, p[b + "ch1.w"], "NN")
+        dx, dgam, dbet = ops.ln_backward_from_cache(g_v, p[b + "ln2.gamma"], *c_ln2, cfg.d_emb)
+        grads[b + "ln2.gamma"] += dgam
+        grads[b + "ln2.beta"] += dbet
+        g_x2 = gh + dx
+        # tok2 (weight-first NT): dW += sum_b g @ a ; ga = g^T W ; db(row) += sum g over E
+        grads[b + "tok2.w"] += _flat(ops.matmul(g_x2, a, "NN"))
+        grads[b + "tok2.b"] += g_x2.sum(axis=tuple(i2 for i2 in range(g_x2.ndim) if i2 != g_x2.ndim - 2))
+        g_t1 = ops.gelu_backward(t1, ops.matmul(g_x2, p[b + "tok2.w"], "TN"))
+        # tok1 (TN): gu = W g^T ; dW += sum_b u @ g ; db += sum over (B, E)
+        grads[b + "tok1.w"] += _flat(ops.matmul(u, g_t1, "NN"))
+        grads[b + "tok1.b"] += g_t1.sum(axis=(0, 1))
+        g_u = ops.matmul(p[b + "tok1.w"], g_t1, "NT")
+        dx, dgam, dbet = ops.ln_backward_from_cache(g_u, p[b + "ln1.gamma"], *c_ln1, cfg.d_emb)
+        grads[b + "ln1.gamma"] += dgam
+        grads[b + "ln1.beta"] += dbet
+        return g_x2 + dx
+
     def forward(self, x, r: int = 1):
         cfg, p = self.cfg, self.p
         xp = ops.patchify(x, *cfg.patch)
@@ -175,18 +216,8 @@ class SerialModel:
         for _ in range(r):
             caches = []
             for i in range(cfg.n_blocks):
-                b = f"block{i}."
-                u, c_ln1 = self._ln(h, b + "ln1.")
-                t1 = ops.matmul(u, p[b + "tok1.w"], "TN") + p[b + "tok1.b"]          # [B, E, K]
-                a = ops.gelu(t1)
-                o = ops.matmul(p[b + "tok2.w"], a, "NT") + p[b + "tok2.b"][:, None]  # [B, T, E]
-                x2 = h + o
-                v, c_ln2 = self._ln(x2, b + "ln2.")
-                cc = ops.matmul(v, p[b + "ch1.w"], "NT") + p[b + "ch1.b"]
-                ca = ops.gelu(cc)
-                z = ops.matmul(ca, p[b + "ch2.w"], "NT") + p[b + "ch2.b"]
-                caches.append((h, c_ln1, u, t1, a, c_ln2, v, cc, ca))
-                h = x2 + z
+                h, cache = self.block_forward(i, h)
+                caches.append(cache)
             passes.append(caches)
         d = ops.matmul(h, p["dec.w"], "NT") + p["dec.b"]
         decoded = ops.unpatchify(d, cfg.grid[0], cfg.grid[1], *cfg.patch)
@@ -211,31 +242,7 @@ class SerialModel:
         gh = ops.matmul(g, p["dec.w"], "NN")
         for caches in reversed(passes):
             for i in reversed(range(cfg.n_blocks)):
-                b = f"block{i}."
-                h, c_ln1, u, t1, a, c_ln2, v, cc, ca = caches[i]
-                # ch2 / ch1 (NT)
-                grads[b + "ch2.w"] += _flat(ops.matmul(gh, ca, "TN"))
-                grads[b + "ch2.b"] += gh.sum(axis=(0, 1))
-                g_c = ops.gelu_backward(cc, ops.matmul(gh, p[b + "ch2.w"], "NN"))
-                grads[b + "ch1.w"] += _flat(ops.matmul(g_c, v, "TN"))
-                grads[b + "ch1.b"] += g_c.sum(axis=(0, 1))
-                g_v = ops.matmul(g_c, p[b + "ch1.w"], "NN")
-                dx, dgam, dbet = ops.ln_backward_from_cache(g_v, p[b + "ln2.gamma"], *c_ln2, cfg.d_emb)
-                grads[b + "ln2.gamma"] += dgam
-                grads[b + "ln2.beta"] += dbet
-                g_x2 = gh + dx
-                # tok2 (weight-first NT): dW += sum_b g @ a ; ga = g^T W ; db(row) += sum g over E
-                grads[b + "tok2.w"] += _flat(ops.matmul(g_x2, a, "NN"))
-                grads[b + "tok2.b"] += g_x2.sum(axis=tuple(i2 for i2 in range(g_x2.ndim) if i2 != g_x2.ndim - 2))
-                g_t1 = ops.gelu_backward(t1, ops.matmul(g_x2, p[b + "tok2.w"], "TN"))
-                # tok1 (TN): gu = W g^T ; dW += sum_b u @ g ; db += sum over (B, E)
-                grads[b + "tok1.w"] += _flat(ops.matmul(u, g_t1, "NN"))
-                grads[b + "tok1.b"] += g_t1.sum(axis=(0, 1))
-                g_u = ops.matmul(p[b + "tok1.w"], g_t1, "NT")
-                dx, dgam, dbet = ops.ln_backward_from_cache(g_u, p[b + "ln1.gamma"], *c_ln1, cfg.d_emb)
-                grads[b + "ln1.gamma"] += dgam
-                grads[b + "ln1.beta"] += dbet
-                gh = g_x2 + dx
+                gh = self.block_backward(i, caches[i], gh, grads)
         grads["enc.w"] += _flat(ops.matmul(gh, xp, "TN"))
         grads["enc.b"] += gh.sum(axis=(0, 1))
         return grads

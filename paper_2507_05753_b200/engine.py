@@ -1,0 +1,105 @@
+"""One WeatherMixer training step as a single CUDA graph (the hot path of BASELINE north_star).
+
+    step = TrainStep(model, batch=1)
+    loss = step(x_host, target_host)        # public API: host buffers in, host loss out
+    step.run_device()                       # inputs already resident (bench `value` leg)
+
+Per step, on one stream: zero gradients (one memset) -> fused forward -> fused blend +
+lat-weighted MSE + its gradient (jg_blend_loss) -> fused backward -> gradient sync of
+duplicated vectors (NCCL, n > 1) -> Adam, one fused kernel per lr class, writing the bf16
+operand copies (jg_adam). The reference has no loss / optimiser; they follow SPEC.md:396-413
+and 482-490 (see train.py).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .model import WeatherMixerModel
+from .train import AdamConfig
+
+
+class TrainStep:
+    def __init__(self, model: WeatherMixerModel, batch: int = 1, r: int = 1, adam: AdamConfig | None = None,
+                 graph: bool = True, loss_scale: float = 1.0):
+        self.model, self.batch, self.r = model, batch, r
+        self.adam = adam or AdamConfig()
+        self.loss_scale = loss_scale
+        self.ws = model.workspace(batch, r)
+        dev = model.device
+        self.target = torch.zeros_like(self.ws.xin)
+        self.step_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.use_graph = graph
+        self.graph = None
+        self.launches_per_step = None
+        self._pinned_loss = torch.zeros(1, dtype=torch.float32, pin_memory=True)
+        self._h2d_bytes = 2 * self.ws.xin.numel() * 4
+        self._d2h_bytes = 4
+
+    # -- the step body --------------------------------------------------------------------
+    def _body(self) -> None:
+        m, ws = self.model, self.ws
+        m.zero_grads()
+        m._forward(ws)
+        ws.loss.zero_()
+        m._blend(ws, target=self.target, loss=ws.loss, loss_scale=self.loss_scale)
+        m._backward(ws)
+        m.grad_sync()
+        self._adam()
+
+    def _adam(self) -> None:
+        f, a = self.model.flat, self.adam
+        _lib.call("jg_step_increment", self.step_count.data_ptr())
+        op_copy = f.op if f.op is not f.master else None
+        for cls, (lo, hi) in f.class_range.items():
+            if hi <= lo:
+                continue
+            _lib.call("jg_adam", f.master[lo:].data_ptr(), f.grad[lo:].data_ptr(), f.m[lo:].data_ptr(),
+                      f.v[lo:].data_ptr(), None if op_copy is None else op_copy[lo:].data_ptr(), hi - lo,
+                      a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count.data_ptr(), None)
+
+    def capture(self) -> None:
+        """Warm up on a side stream, then capture the step into a CUDA graph."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            before = _lib.launch_count()
+            self._body()
+            self.launches_per_step = _lib.launch_count() - before
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        # the warm-up was a real training step (Adam state and step counter advanced)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._body()
+        self.graph = g
+        torch.cuda.synchronize()
+
+    def run_device(self) -> torch.Tensor:
+        """One step on resident inputs (self.ws.xin / self.target); returns the device loss."""
+        if self.use_graph:
+            if self.graph is None:
+                self.capture()
+            self.graph.replay()
+        else:
+            before = _lib.launch_count()
+            self._body()
+            self.launches_per_step = _lib.launch_count() - before
+        return self.ws.loss
+
+    def __call__(self, x: torch.Tensor, target: torch.Tensor) -> float:
+        """Public step: copy this step's inputs from (pinned) host memory, run, read the loss."""
+        self.ws.xin.copy_(x, non_blocking=True)
+        self.target.copy_(target, non_blocking=True)
+        loss = self.run_device()
+        self._pinned_loss.copy_(loss, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return float(self._pinned_loss.item())
+
+    @property
+    def h2d_bytes_per_step(self) -> int:
+        return self._h2d_bytes
+
+    @property
+    def d2h_bytes_per_step(self) -> int:
+        return self._d2h_bytes

@@ -25,6 +25,10 @@ from .errors import ShapeError
 
 DTYPES = {"f32": torch.float32, "bf16": torch.bfloat16}
 
+# Optional per-launch GEMM timer (bench.py roofline leg): a list collecting
+# (start_event, end_event, algorithmic_flops) for every jg_gemm launch while set.
+GEMM_TIMER: list | None = None
+
 
 class MatmulMode(str, enum.Enum):
     """The three layer multiplication layouts: X@W, X@W.T and X.T@W (tensor.py:27-33)."""
@@ -114,7 +118,14 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
         d.pre, d.ldp, d.p_bstride, d.pre_type = pre.data_ptr(), n, p_bs if p_bs else m * n, _lib.dtype_code(pre)
     if stats is not None:
         d.stats, d.stats_bstride = stats.data_ptr(), stats_bs if stats_bs else 2 * m
-    _lib.gemm_raw(d)
+    if GEMM_TIMER is not None:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        _lib.gemm_raw(d)
+        e.record()
+        GEMM_TIMER.append((s, e, 2 * m * n * k * batch))
+    else:
+        _lib.gemm_raw(d)
     return out
 
 
