@@ -88,6 +88,17 @@ typedef struct jg_gemm_desc {
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);
 
+/*
+ * jg_epilogue — the jg_gemm epilogue (same descriptor fields: m, n, batch, epi, alpha, d, d2,
+ * bias, resid, pre, stats; A/B fields ignored) applied to an fp32 accumulator acc[b][m][lda]
+ * that arrived by another route: the NCCL reduce-scatter of Jigsaw partial products
+ * (parallel.py:118-132 sums partials; the bias/GELU/residual follow, parallel.py:521-525).
+ */
+int jg_epilogue(const jg_gemm_desc* desc, const float* acc, int64_t lda, int64_t acc_bstride, void* stream);
+
+/* y += alpha * x (fp32): accumulate a reduce-scattered weight gradient (parallel.py:490-493). */
+int jg_axpy(float* y, const float* x, float alpha, int64_t n, void* stream);
+
 /* Split fp32 x into tf32-exact hi (low 13 mantissa bits cleared) and lo = x - hi. */
 int jg_split_tf32(const float* x, float* hi, float* lo, int64_t n, void* stream);
 

@@ -436,6 +436,59 @@ __global__ void sqnorm_kernel(const float* __restrict__ x, int64_t n, float* __r
   }
 }
 
+// ---------------------------------------------------------------- standalone epilogue
+// The jg_gemm epilogue applied to an fp32 accumulator that arrived by another route (an NCCL
+// reduce-scatter of Jigsaw partial products). Warp per row, lanes over columns.
+struct EpiArgs {
+  int64_t m, n;
+  uint32_t epi;
+  float alpha;
+  const float* acc; int64_t lda, a_bs;
+  void* d; int64_t ldd, d_bs; bool d_bf16;
+  void* d2; int64_t ldd2, d2_bs; bool d2_bf16;
+  const float* bias; int64_t bias_bs;
+  const float* resid; int64_t ldr, r_bs;
+  const void* pre; int64_t ldp, p_bs; bool pre_bf16;
+  float* stats; int64_t stats_bs;
+};
+
+__global__ void epilogue_kernel(const EpiArgs a) {
+  const int64_t b = blockIdx.y;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < a.m; r += warps) {
+    const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
+    float s1 = 0.f, s2 = 0.f;
+    for (int64_t c = lane; c < a.n; c += 32) {
+      float v = a.alpha * a.acc[b * a.a_bs + r * a.lda + c];
+      if (a.epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
+      v += rb;
+      if (a.epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
+      if (a.epi & JG_EPI_GELU_BWD) v *= jgd::gelu_grad_f(jgd::load1(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16));
+      const int64_t od = b * a.d_bs + r * a.ldd + c;
+      if (a.epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
+      s1 += v;
+      s2 += v * v;
+      if (a.d) jgd::store1(a.d, od, a.d_bf16, v);
+      if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
+        jgd::store1(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
+    }
+    if (a.epi & JG_EPI_STATS) {
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        atomicAdd(a.stats + b * a.stats_bs + 2 * r, s1);
+        atomicAdd(a.stats + b * a.stats_bs + 2 * r + 1, s2);
+      }
+    }
+  }
+}
+
+__global__ void axpy_kernel(float* __restrict__ y, const float* __restrict__ x, float alpha, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += alpha * x[i];
+}
+
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
@@ -617,6 +670,36 @@ int jg_sqnorm(const float* x, int64_t n, float* out, void* stream) {
   if (n == 0) return JG_OK;
   sqnorm_kernel<<<grid_for(n, 1024), 256, 0, (cudaStream_t)stream>>>(x, n, out);
   JG_LAUNCH_CHECK("sqnorm");
+  return JG_OK;
+}
+
+int jg_epilogue(const jg_gemm_desc* g, const float* acc, int64_t lda, int64_t acc_bstride, void* stream) {
+  JG_SHAPE_CHECK(g && acc && g->m > 0 && g->n > 0 && g->batch > 0, "jg_epilogue: bad shape");
+  JG_SHAPE_CHECK(!(g->epi & JG_EPI_ACCUM) || (g->d && g->d_type == JG_F32), "jg_epilogue: ACCUM needs an fp32 D");
+  JG_SHAPE_CHECK(!(g->epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) || g->d2, "jg_epilogue: missing D2");
+  JG_SHAPE_CHECK(!(g->epi & (JG_EPI_BIAS_COL | JG_EPI_BIAS_ROW)) || g->bias, "jg_epilogue: missing bias");
+  JG_SHAPE_CHECK(!(g->epi & JG_EPI_RESID) || g->resid, "jg_epilogue: missing resid");
+  JG_SHAPE_CHECK(!(g->epi & JG_EPI_GELU_BWD) || g->pre, "jg_epilogue: missing pre");
+  JG_SHAPE_CHECK(!(g->epi & JG_EPI_STATS) || g->stats, "jg_epilogue: missing stats");
+  EpiArgs a;
+  a.m = g->m; a.n = g->n; a.epi = g->epi; a.alpha = g->alpha;
+  a.acc = acc; a.lda = lda; a.a_bs = acc_bstride;
+  a.d = g->d; a.ldd = g->ldd; a.d_bs = g->d_bstride; a.d_bf16 = g->d_type == JG_BF16;
+  a.d2 = g->d2; a.ldd2 = g->ldd2; a.d2_bs = g->d2_bstride; a.d2_bf16 = g->d2_type == JG_BF16;
+  a.bias = g->bias; a.bias_bs = g->bias_bstride;
+  a.resid = g->resid; a.ldr = g->ldr; a.r_bs = g->r_bstride;
+  a.pre = g->pre; a.ldp = g->ldp; a.p_bs = g->p_bstride; a.pre_bf16 = g->pre_type == JG_BF16;
+  a.stats = g->stats; a.stats_bs = g->stats_bstride;
+  dim3 grid((unsigned)grid_for(g->m, 8), (unsigned)g->batch);
+  epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  JG_LAUNCH_CHECK("epilogue");
+  return JG_OK;
+}
+
+int jg_axpy(float* y, const float* x, float alpha, int64_t n, void* stream) {
+  if (n == 0) return JG_OK;
+  axpy_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(y, x, alpha, n);
+  JG_LAUNCH_CHECK("axpy");
   return JG_OK;
 }
 

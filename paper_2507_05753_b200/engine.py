@@ -15,6 +15,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib
+from . import kernels as K
 from .model import WeatherMixerModel
 from .train import AdamConfig
 
@@ -43,20 +44,21 @@ class TrainStep:
         m._forward(ws)
         ws.loss.zero_()
         m._blend(ws, target=self.target, loss=ws.loss, loss_scale=self.loss_scale)
+        if m.ctx.n > 1:
+            m.ctx.all_reduce_all(ws.loss)  # the loss is a sum of per-tile terms
         m._backward(ws)
         m.grad_sync()
         self._adam()
 
     def _adam(self) -> None:
         f, a = self.model.flat, self.adam
-        _lib.call("jg_step_increment", self.step_count.data_ptr())
+        K.step_increment(self.step_count)
         op_copy = f.op if f.op is not f.master else None
         for cls, (lo, hi) in f.class_range.items():
             if hi <= lo:
                 continue
-            _lib.call("jg_adam", f.master[lo:].data_ptr(), f.grad[lo:].data_ptr(), f.m[lo:].data_ptr(),
-                      f.v[lo:].data_ptr(), None if op_copy is None else op_copy[lo:].data_ptr(), hi - lo,
-                      a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count.data_ptr(), None)
+            K.adam(f.master[lo:], f.grad[lo:], f.m[lo:], f.v[lo:], None if op_copy is None else op_copy[lo:],
+                   hi - lo, a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count)
 
     def capture(self) -> None:
         """Warm up on a side stream, then capture the step into a CUDA graph."""

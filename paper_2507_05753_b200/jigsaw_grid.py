@@ -1,0 +1,259 @@
+"""Jigsaw R x C execution of the WeatherMixer step (n = 2, 4, 8 GPUs).
+
+Rank (r, c) of the grid (r: longitude part / token set, c: channel part) holds
+
+  activations x, u, v, x2      [B, T_r, E/C]          patch features  [B, T_r, F/C]
+  tok1 output h, gelu(h)       [B, E/R, d_tok/C]      ch1 output      [B, T_r, d_ch/C]
+  enc.w [E/R, F/C]  tok1.w, tok2.w [T_r, d_tok/C]  ch1.w [d_ch/R, E/C]  ch2.w [E/R, d_ch/C]
+  dec.w [F/R, E/C]  column vectors [./C] (shared by the column group), tok2.b [T_r] (row group)
+
+so no weight or activation element is stored twice (the vectors excepted, as in the
+reference, model.py:168-173). With (R, C) = (1, 2) / (2, 2) these are exactly the reference's
+n = 2 / n = 4 tiles (model.py:135-150); (4, 2) is the 8-way grid.
+
+Every layer is "gather one operand along one grid axis -> one local tcgen05 GEMM (1/n of the
+FLOPs) -> reduce-scatter the fp32 partials along the other axis", replacing the reference's
+point-to-point schedules (parallel.py:118-353) whose 4-way version is FLOP-imbalanced 1:3:3:1:
+
+  channel NT (enc, ch1, ch2, dec)   fwd: W panel AG(col) at step start; GEMM -> [C][M][N/C]
+                                         partials; RS(row); jg_epilogue (bias/GELU/residual/
+                                         LN moments)
+                                    bwd: AG(row) dY; dX = sum_j dY_j W_j (batch-reduced GEMM,
+                                         GELU' fused); dW partial -> RS(col)
+  tok1 TN  h = u^T W1               fwd: AG(row) u; GEMM -> [E, K/C] partial; RS(col)
+  tok2 NT  o = W2 a^T               fwd: AG(col) a; GEMM -> [C][T_r][E/C]; RS(row)
+  layer norm over split E           row moments all-reduced over the row group (stats_peer,
+                                    model.py:220-231)
+  duplicated-vector gradients       one all-reduce per (lr class, vector kind) (model.py:451-460)
+
+Collectives are NCCL (torch.distributed) on the compute stream, so the whole step stays one
+CUDA graph.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from . import kernels as K
+
+KM, MN = _lib.JG_KMAJOR, _lib.JG_MNMAJOR
+E_ACC, E_BCOL, E_BROW, E_RES = _lib.EPI_ACCUM, _lib.EPI_BIAS_COL, _lib.EPI_BIAS_ROW, _lib.EPI_RESID
+E_GF, E_GB, E_CP, E_ST = _lib.EPI_GELU_FWD, _lib.EPI_GELU_BWD, _lib.EPI_COPY_D2, _lib.EPI_STATS
+
+CHANNEL_LAYERS = ("enc.w", "ch1.w", "ch2.w", "dec.w")
+
+
+class GridWorkspace:
+    """Gathered panels and collective scratch for one (batch, rollout) shape."""
+
+    def __init__(self, m, ws):
+        cfg, dev = m.cfg, m.device
+        R, C = m.R, m.C
+        B, nj = ws.B, ws.r * cfg.n_blocks
+        E, H, F, Kd = cfg.d_emb, cfg.d_ch, cfg.patch_features, cfg.d_tok
+        Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
+        M = B * Tl
+        od = m.op_dtype
+        f32 = dict(dtype=torch.float32, device=dev)
+        opk = dict(dtype=od, device=dev)
+        self.R, self.C = R, C
+        # weight panels: W rows gathered over the column group [N_out, K_in / C]
+        self.panel_shape = {"enc.w": (E, Fl), "ch1.w": (H, El), "ch2.w": (E, Hl), "dec.w": (F, El)}
+        self.panels = {}
+        for name in m.params:
+            base = name.split(".", 1)[-1] if name.startswith("block") else name
+            if base in CHANNEL_LAYERS and R > 1:
+                self.panels[name] = torch.empty(self.panel_shape[base], **opk)
+        nmax = max(E, H, F)
+        kin_max = max(E * Fl, H * El, E * Hl, F * El)
+        self.scratch = torch.empty(max(M * nmax, kin_max, Tl * E, E * Kl), **f32)
+        self.red = torch.empty(max(M * nmax // C, kin_max // R, Er * Kl, Tl * El), **f32)
+        self.op_scratch = torch.empty(max(M * nmax, Tl * E), **opk)
+        self.op_scratch2 = torch.empty(Tl * E, **opk)
+        self.gh_col = torch.empty(E * Kl, **opk)
+        self.u_row = [torch.empty((B, C, Tl, El), **opk) for _ in range(nj)]
+        self.a_col = [torch.empty((B, E, Kl), **opk) for _ in range(nj)] if R > 1 else None
+
+
+def _gw(m, ws) -> GridWorkspace:
+    if getattr(ws, "grid", None) is None:
+        ws.grid = GridWorkspace(m, ws)
+    return ws.grid
+
+
+def _panel(m, g, name):
+    return g.panels[name] if m.R > 1 else m.params[name].op
+
+
+def gather_panels(m, g) -> None:
+    """All-gather every channel-mixing weight over the column group (weights are final for the step)."""
+    for name, buf in g.panels.items():
+        m.ctx.ag_col_into(buf, m.params[name].op)
+
+
+# --------------------------------------------------------------------------- channel layers
+def chan_fwd(m, g, X, panel, M, kin_l, nout, **epi):
+    """Y[M, nout/C] = X[M, kin_l] W^T (+ epilogue), W panel [nout, kin_l]."""
+    C = m.C
+    nl = nout // C
+    P = g.scratch[:C * M * nl].view(C, M, nl)
+    K.gemm(P, X, panel, KM, KM, M, nl, kin_l, C, 0, nl * kin_l, d_bs=M * nl)
+    red = g.red[:M * nl].view(M, nl)
+    m.ctx.rs_row_into(red, P)
+    K.epilogue(red, M, nl, **epi)
+
+
+def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None, **dx_epi):
+    """Backward of Y = X W^T: dX (optional, fused epilogue), dW (+= via RS over the column group),
+    bias gradient partial (summed over the column group in grad_sync)."""
+    R, C = m.R, m.C
+    nl = nout // C
+    dyrow = g.op_scratch[:C * M * nl].view(C, M, nl)
+    m.ctx.ag_row_into(dyrow, dY)
+    if dX is not None:
+        K.gemm(dX, dyrow, panel, KM, MN, M, kin_l, nl, C, M * nl, nl * kin_l, reduce_batch=True, **dx_epi)
+    wgrad = m.params[wname].grad
+    if R == 1:
+        K.gemm(wgrad, dyrow, X, MN, MN, nl, kin_l, M, C, M * nl, 0, d_bs=nl * kin_l, epi=E_ACC)
+    else:
+        P = g.scratch[:nout * kin_l].view(C, nl, kin_l)
+        K.gemm(P, dyrow, X, MN, MN, nl, kin_l, M, C, M * nl, 0, d_bs=nl * kin_l)
+        red = g.red[:(nout // R) * kin_l].view(nout // R, kin_l)
+        m.ctx.rs_col_into(red, P.view(R, nout // R, kin_l))
+        K.axpy(wgrad, red)
+    K.colsum(bias_src, m.params[bname].grad, M, nl)
+
+
+# --------------------------------------------------------------------------- forward
+def forward_grid(m, ws) -> None:
+    g = _gw(m, ws)
+    cfg, p, ctx = m.cfg, m.params, m.ctx
+    R, C = m.R, m.C
+    B = ws.B
+    E, H, F = cfg.d_emb, cfg.d_ch, cfg.patch_features
+    Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
+    M = B * Tl
+    lat, lon = m.local_grid
+    ws.stats.zero_()
+    gather_panels(m, g)
+    K.patchify(ws.xin, ws.xp, B, lat, lon, m.local_vars, cfg.patch[0], cfg.patch[1])
+    chan_fwd(m, g, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, epi=E_BCOL | E_ST, bias=p["enc.b"].data,
+             d=ws.res[0], stats=ws.st1[0])
+    nj = ws.r * cfg.n_blocks
+    for j in range(nj):
+        b = f"block{j % cfg.n_blocks}."
+        ctx.all_reduce_row(ws.st1[j])
+        K.ln_apply(ws.res[j], ws.st1[j], p[b + "ln1.gamma"].data, p[b + "ln1.beta"].data, ws.u[j], ws.mr1[j],
+                   M, El, E, m.eps)
+        for bi in range(B):
+            # tok1: h = u^T W1 + b1 ; a = gelu(h)            rows of h: E (gathered), split R ways
+            urow = g.u_row[j][bi]
+            ctx.ag_row_into(urow, ws.u[j][bi])
+            if R == 1:
+                K.gemm(ws.h[j][bi], urow, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
+                       epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d2=ws.a[j][bi], d2_bs=El * Kl)
+            else:
+                P = g.scratch[:E * Kl].view(C, El, Kl)
+                K.gemm(P, urow, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl)
+                red = g.red[:Er * Kl].view(Er, Kl)
+                ctx.rs_col_into(red, P.view(R, Er, Kl))
+                K.epilogue(red, Er, Kl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d=ws.h[j][bi], d2=ws.a[j][bi])
+            # tok2: x2 = x + W2 a^T + b2[:, None]             a gathered over the column group
+            if R > 1:
+                acol = g.a_col[j][bi]
+                ctx.ag_col_into(acol, ws.a[j][bi])
+            else:
+                acol = ws.a[j][bi]
+            P = g.scratch[:C * Tl * El].view(C, Tl, El)
+            K.gemm(P, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=Tl * El)
+            red = g.red[:Tl * El].view(Tl, El)
+            ctx.rs_row_into(red, P)
+            K.epilogue(red, Tl, El, epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data, resid=ws.res[j][bi],
+                       d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
+        ctx.all_reduce_row(ws.st2[j])
+        K.ln_apply(ws.x2[j], ws.st2[j], p[b + "ln2.gamma"].data, p[b + "ln2.beta"].data, ws.v[j], ws.mr2[j],
+                   M, El, E, m.eps)
+        chan_fwd(m, g, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, epi=E_BCOL | E_GF,
+                 bias=p[b + "ch1.b"].data, d=ws.c[j], d2=ws.ca[j])
+        last = j == nj - 1
+        copy_y = last and ws.y_op is not ws.res[nj]
+        chan_fwd(m, g, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E,
+                 epi=E_BCOL | E_RES | (E_CP if copy_y else 0) | (0 if last else E_ST), bias=p[b + "ch2.b"].data,
+                 resid=ws.x2[j], d=ws.res[j + 1], d2=ws.y_op if copy_y else None,
+                 stats=None if last else ws.st1[j + 1])
+    chan_fwd(m, g, ws.y_op, _panel(m, g, "dec.w"), M, El, F, epi=E_BCOL, bias=p["dec.b"].data, d=ws.dec)
+
+
+# --------------------------------------------------------------------------- backward
+def backward_grid(m, ws) -> None:
+    g = _gw(m, ws)
+    cfg, p, ctx = m.cfg, m.params, m.ctx
+    R, C = m.R, m.C
+    B = ws.B
+    E, H, F = cfg.d_emb, cfg.d_ch, cfg.patch_features
+    Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
+    M = B * Tl
+    ws.bstats.zero_()
+    gf, gop = ws.g, ws.g_op
+    # decoder: g = gd Wdec (+ bf16 copy)
+    cp = gop is not gf
+    chan_bwd(m, g, ws.gd, ws.y_op, _panel(m, g, "dec.w"), M, El, F, "dec.w", "dec.b", ws.gd, dX=gf,
+             epi=E_CP if cp else 0, d2=gop if cp else None)
+    nj = ws.r * cfg.n_blocks
+    for j in reversed(range(nj)):
+        b = f"block{j % cfg.n_blocks}."
+        # ch2: gc = (g Wc2) * gelu'(c)
+        chan_bwd(m, g, gop, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b", gf,
+                 dX=ws.gc, epi=E_GB, pre=ws.c[j])
+        # ch1: gv = gc Wc1
+        chan_bwd(m, g, ws.gc, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, b + "ch1.w", b + "ch1.b", ws.gc,
+                 dX=ws.gv)
+        m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, ws.gx2_op, M, El, E,
+                  row_reduce=ctx.all_reduce_row)
+        for bi in range(B):
+            # tok2 backward: dW2 += sum_e g_x2 a ; gh = (g_x2^T W2) * gelu'(h)
+            grow = g.op_scratch2[:C * Tl * El].view(C, Tl, El)
+            ctx.ag_row_into(grow, ws.gx2_op[bi])
+            acol = g.a_col[j][bi] if R > 1 else ws.a[j][bi]
+            K.gemm(p[b + "tok2.w"].grad, grow, acol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True,
+                   epi=E_ACC)
+            K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
+            if R == 1:
+                K.gemm(ws.gh[bi], grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
+                       epi=E_GB, pre=ws.h[j][bi])
+            else:
+                P = g.scratch[:E * Kl].view(C, El, Kl)
+                K.gemm(P, grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl)
+                red = g.red[:Er * Kl].view(Er, Kl)
+                ctx.rs_col_into(red, P.view(R, Er, Kl))
+                K.epilogue(red, Er, Kl, epi=E_GB, pre=ws.h[j][bi], d=ws.gh[bi])
+        K.colsum(ws.gh, p[b + "tok1.b"].grad, B * Er, Kl)
+        for bi in range(B):
+            # tok1 backward: gu = W1 gh^T (RS over the row group) ; dW1 += sum_e u gh
+            if R > 1:
+                ghcol = g.gh_col[:E * Kl].view(E, Kl)
+                ctx.ag_col_into(ghcol, ws.gh[bi])
+            else:
+                ghcol = ws.gh[bi]
+            P = g.scratch[:C * Tl * El].view(C, Tl, El)
+            K.gemm(P, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=Tl * El)
+            ctx.rs_row_into(ws.gu[bi], P)
+            K.gemm(p[b + "tok1.w"].grad, g.u_row[j][bi], ghcol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl,
+                   reduce_batch=True, epi=E_ACC)
+        m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, gop, M, El, E,
+                  row_reduce=ctx.all_reduce_row)
+    # encoder: dW only (the input gradient is not needed, model.py:444-445)
+    chan_bwd(m, g, gop, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, "enc.w", "enc.b", gf)
+
+
+def grad_sync(m) -> None:
+    """Sum duplicated-vector gradients over their sharing group: column vectors over the column
+    group, the tok2 row bias over the row group (model.py:451-460) — one all-reduce per range."""
+    f, ctx = m.flat, m.ctx
+    for cls in f.CLASSES:
+        lo, hi = f.kind_range[(cls, "vec_col")]
+        if hi > lo and m.R > 1:
+            ctx.all_reduce_col(f.grad[lo:hi])
+        lo, hi = f.kind_range[(cls, "vec_row")]
+        if hi > lo and m.C > 1:
+            ctx.all_reduce_row(f.grad[lo:hi])

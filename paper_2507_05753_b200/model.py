@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from . import tensor as T
+from . import kernels as K
 from .config import ConfigError, ModelConfig, token_sets  # noqa: F401  (re-exported)
 from .errors import ShapeError
 from .params import FlatParams, Param
@@ -145,9 +145,9 @@ class WeatherMixerModel:
         # axis splits (model.py:316-321): strided longitude token sets, contiguous channel chunks
         self.t_sets = token_sets(cfg, self.R) if self.R > 1 else [np.arange(cfg.tokens)]
         split = lambda size, parts: contiguous_split(size, parts) if parts > 1 else [np.arange(size)]  # noqa: E731
-        E, K, H, F = cfg.d_emb, cfg.d_tok, cfg.d_ch, cfg.patch_features
+        E, Kd, H, F = cfg.d_emb, cfg.d_tok, cfg.d_ch, cfg.patch_features
         self.sets = {
-            "T": self.t_sets, "E_R": split(E, self.R), "E_C": split(E, self.C), "K_C": split(K, self.C),
+            "T": self.t_sets, "E_R": split(E, self.R), "E_C": split(E, self.C), "K_C": split(Kd, self.C),
             "H_R": split(H, self.R), "H_C": split(H, self.C), "F_R": split(F, self.R), "F_C": split(F, self.C),
             "V_C": split(cfg.n_vars, self.C),
         }
@@ -157,7 +157,7 @@ class WeatherMixerModel:
         local_specs = []
         for name, gshape, _, kind, rs, cs, lr_class, _ in self._specs:
             lay = self.layouts[name]
-            local_specs.append((name, self._local_shape(lay), lr_class, lay.dup_positions(ctx.pos)))
+            local_specs.append((name, self._local_shape(lay), lr_class, lay.dup_positions(ctx.pos), kind))
         self.flat = FlatParams(local_specs, self.device, self.op_dtype)
         self.params: dict[str, Param] = self.flat.params
         self._init(init)
@@ -167,7 +167,7 @@ class WeatherMixerModel:
     # -- registration (model.py:336-389) --------------------------------------------------
     def _register_all(self):
         cfg, s, n = self.cfg, self.sets, self.ctx.n
-        E, K, H, F, Tn, Cv = cfg.d_emb, cfg.d_tok, cfg.d_ch, cfg.patch_features, cfg.tokens, cfg.n_vars
+        E, Kd, H, F, Tn, Cv = cfg.d_emb, cfg.d_tok, cfg.d_ch, cfg.patch_features, cfg.tokens, cfg.n_vars
 
         def weight(name, shape, fan_in, row_sets, col_sets, lr_class="body"):
             self.layouts[name] = Layout(n, "matrix", shape, row_sets, col_sets)
@@ -184,9 +184,9 @@ class WeatherMixerModel:
             p = f"block{i}."
             vec(p + "ln1.gamma", E, s["E_C"], "vec_col", init=1.0)
             vec(p + "ln1.beta", E, s["E_C"], "vec_col")
-            weight(p + "tok1.w", (Tn, K), Tn, s["T"], s["K_C"])
-            vec(p + "tok1.b", K, s["K_C"], "vec_col")
-            weight(p + "tok2.w", (Tn, K), K, s["T"], s["K_C"])
+            weight(p + "tok1.w", (Tn, Kd), Tn, s["T"], s["K_C"])
+            vec(p + "tok1.b", Kd, s["K_C"], "vec_col")
+            weight(p + "tok2.w", (Tn, Kd), Kd, s["T"], s["K_C"])
             vec(p + "tok2.b", Tn, s["T"], "vec_row")
             vec(p + "ln2.gamma", E, s["E_C"], "vec_col", init=1.0)
             vec(p + "ln2.beta", E, s["E_C"], "vec_col")
@@ -237,7 +237,7 @@ class WeatherMixerModel:
     def sync_operand_copies(self):
         """Refresh the bf16 GEMM-operand copy of the master weights (after init / external edits)."""
         if self.flat.op is not self.flat.master:
-            _lib.call("jg_cast_bf16", self.flat.master.data_ptr(), self.flat.op.data_ptr(), self.flat.total)
+            K.cast_bf16(self.flat.master, self.flat.op)
 
     # -- introspection (model.py:462-529) -------------------------------------------------
     @property
@@ -344,18 +344,17 @@ class WeatherMixerModel:
 
     # ======================================================================= kernels (n = 1)
     def _gemm(self, out, a, b, am, bm, m, n, k, *batch_args, **kw):
-        T.gemm_into(out, a, b, am, bm, m, n, k, *batch_args, **kw)
+        K.gemm(out, a, b, am, bm, m, n, k, *batch_args, **kw)
 
     def _forward(self, ws: "_Workspace") -> None:
         if self.ctx.n > 1:
             return self._forward_grid(ws)
         cfg, p, B = self.cfg, self.params, ws.B
-        Tn, E, F, K, H = cfg.tokens, cfg.d_emb, cfg.patch_features, cfg.d_tok, cfg.d_ch
+        Tn, E, F, Kd, H = cfg.tokens, cfg.d_emb, cfg.patch_features, cfg.d_tok, cfg.d_ch
         lat, lon = self.local_grid
         M = B * Tn
         ws.stats.zero_()
-        _lib.call("jg_patchify", ws.xin.data_ptr(), ws.xp.data_ptr(), _lib.dtype_code(ws.xp), B, lat, lon,
-                  cfg.n_vars, cfg.patch[0], cfg.patch[1])
+        K.patchify(ws.xin, ws.xp, B, lat, lon, cfg.n_vars, cfg.patch[0], cfg.patch[1])
         # encoder: res0 = xp Wenc^T + benc, with LN1 moments of block 0
         self._gemm(ws.res[0], ws.xp, p["enc.w"].op, KM, KM, M, E, F, epi=E_BCOL | E_ST,
                    bias=p["enc.b"].data, stats=ws.st1[0])
@@ -363,19 +362,17 @@ class WeatherMixerModel:
         for j in range(nj):
             b = f"block{j % cfg.n_blocks}."
             x = ws.res[j]
-            _lib.call("jg_ln_apply", x.data_ptr(), ws.st1[j].data_ptr(), p[b + "ln1.gamma"].data.data_ptr(),
-                      p[b + "ln1.beta"].data.data_ptr(), ws.u[j].data_ptr(), _lib.dtype_code(ws.u[j]),
-                      ws.mr1[j].data_ptr(), M, E, E, self.eps)
+            K.ln_apply(x, ws.st1[j], p[b + "ln1.gamma"].data, p[b + "ln1.beta"].data, ws.u[j], ws.mr1[j], M, E, E,
+                       self.eps)
             # tok1 (TN, per sample): h = u^T W1 + b1 ; a = gelu(h)
-            self._gemm(ws.h[j], ws.u[j], p[b + "tok1.w"].op, MN, MN, E, K, Tn, B, Tn * E, 0,
+            self._gemm(ws.h[j], ws.u[j], p[b + "tok1.w"].op, MN, MN, E, Kd, Tn, B, Tn * E, 0,
                        epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d2=ws.a[j])
             # tok2 (weight-first NT): x2 = x + W2 a^T + b2[:, None] ; LN2 moments
-            self._gemm(ws.x2[j], p[b + "tok2.w"].op, ws.a[j], KM, KM, Tn, E, K, B, 0, E * K,
+            self._gemm(ws.x2[j], p[b + "tok2.w"].op, ws.a[j], KM, KM, Tn, E, Kd, B, 0, E * Kd,
                        epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data, resid=x, stats=ws.st2[j],
                        stats_bs=2 * Tn)
-            _lib.call("jg_ln_apply", ws.x2[j].data_ptr(), ws.st2[j].data_ptr(), p[b + "ln2.gamma"].data.data_ptr(),
-                      p[b + "ln2.beta"].data.data_ptr(), ws.v[j].data_ptr(), _lib.dtype_code(ws.v[j]),
-                      ws.mr2[j].data_ptr(), M, E, E, self.eps)
+            K.ln_apply(ws.x2[j], ws.st2[j], p[b + "ln2.gamma"].data, p[b + "ln2.beta"].data, ws.v[j], ws.mr2[j],
+                       M, E, E, self.eps)
             # ch1: c = v Wc1^T + bc1 ; ca = gelu(c)
             self._gemm(ws.c[j], ws.v[j], p[b + "ch1.w"].op, KM, KM, M, H, E, epi=E_BCOL | E_GF,
                        bias=p[b + "ch1.b"].data, d2=ws.ca[j])
@@ -393,27 +390,22 @@ class WeatherMixerModel:
         """Decoder tail: unpatchify + blend (+ loss and its gradient, or an external gradient)."""
         cfg = self.cfg
         lat, lon = self.local_grid
-        p = self.params
-        bw = p["blend.w"]
+        bw = self.params["blend.w"]
         want_grad = g_ext is not None or target is not None
-        _lib.call("jg_blend_loss", ws.dec.data_ptr(), ws.xin.data_ptr(), _lib.ptr(target), bw.data.data_ptr(),
-                  ws.lat_w.data_ptr(), ws.var_w.data_ptr(), _lib.ptr(g_ext), _lib.ptr(out), _lib.ptr(loss),
-                  bw.grad.data_ptr() if want_grad else None,
-                  ws.gd.data_ptr() if want_grad and ws.gd.dtype == torch.float32 else None,
-                  ws.gd.data_ptr() if want_grad and ws.gd.dtype == torch.bfloat16 else None,
-                  ws.B, lat, lon, self.local_vars, cfg.patch[0], cfg.patch[1], float(ws.inv_count), float(loss_scale))
+        K.blend_loss(ws.dec, ws.xin, target, bw.data, ws.lat_w, ws.var_w, g_ext, out, loss,
+                     bw.grad if want_grad else None, ws.gd if want_grad else None, ws.B, lat, lon, self.local_vars,
+                     cfg.patch[0], cfg.patch[1], ws.inv_count, loss_scale)
 
     def _backward(self, ws: "_Workspace") -> None:
         if self.ctx.n > 1:
             return self._backward_grid(ws)
         cfg, p, B = self.cfg, self.params, ws.B
-        Tn, E, F, K, H = cfg.tokens, cfg.d_emb, cfg.patch_features, cfg.d_tok, cfg.d_ch
+        Tn, E, F, Kd, H = cfg.tokens, cfg.d_emb, cfg.patch_features, cfg.d_tok, cfg.d_ch
         M = B * Tn
-        opc = _lib.dtype_code(ws.g_op)
         ws.bstats.zero_()
         # decoder (NT): dW += gd^T y ; db += sum gd ; g = gd Wdec
         self._gemm(p["dec.w"].grad, ws.gd, ws.y_op, MN, MN, F, E, M, epi=E_ACC)
-        _lib.call("jg_colsum", ws.gd.data_ptr(), _lib.dtype_code(ws.gd), p["dec.b"].grad.data_ptr(), M, F, F)
+        K.colsum(ws.gd, p["dec.b"].grad, M, F)
         g, g_op = ws.g, ws.g_op
         self._gemm(g, ws.gd, p["dec.w"].op, KM, MN, M, E, F, epi=0 if g_op is g else E_CP,
                    d2=None if g_op is g else g_op)
@@ -422,41 +414,41 @@ class WeatherMixerModel:
             b = f"block{j % cfg.n_blocks}."
             # ch2: dWc2 += g^T ca ; dbc2 += sum g ; gc = (g Wc2) * gelu'(c)
             self._gemm(p[b + "ch2.w"].grad, g_op, ws.ca[j], MN, MN, E, H, M, epi=E_ACC)
-            _lib.call("jg_colsum", g.data_ptr(), _lib.JG_F32, p[b + "ch2.b"].grad.data_ptr(), M, E, E)
+            K.colsum(g, p[b + "ch2.b"].grad, M, E)
             self._gemm(ws.gc, g_op, p[b + "ch2.w"].op, KM, MN, M, H, E, epi=E_GB, pre=ws.c[j])
             # ch1: dWc1 += gc^T v ; dbc1 += sum gc ; gv = gc Wc1
             self._gemm(p[b + "ch1.w"].grad, ws.gc, ws.v[j], MN, MN, H, E, M, epi=E_ACC)
-            _lib.call("jg_colsum", ws.gc.data_ptr(), _lib.dtype_code(ws.gc), p[b + "ch1.b"].grad.data_ptr(), M, H, H)
+            K.colsum(ws.gc, p[b + "ch1.b"].grad, M, H)
             self._gemm(ws.gv, ws.gc, p[b + "ch1.w"].op, KM, MN, M, E, H)
             # ln2 backward + residual: g_x2 = g + LN2'(gv)
             self._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], g, ws.gx2, ws.gx2_op, M, E)
             # tok2 (weight-first): dW2 += sum_b g_x2 a ; db2 += row sums ; gh = (g_x2^T W2) * gelu'(h)
-            self._gemm(p[b + "tok2.w"].grad, ws.gx2_op, ws.a[j], KM, MN, Tn, K, E, B, Tn * E, E * K,
+            self._gemm(p[b + "tok2.w"].grad, ws.gx2_op, ws.a[j], KM, MN, Tn, Kd, E, B, Tn * E, E * Kd,
                        reduce_batch=True, epi=E_ACC)
             for bi in range(B):
-                _lib.call("jg_rowsum", ws.gx2[bi].data_ptr(), _lib.JG_F32, p[b + "tok2.b"].grad.data_ptr(), Tn, E, E)
-            self._gemm(ws.gh, ws.gx2_op, p[b + "tok2.w"].op, MN, MN, E, K, Tn, B, Tn * E, 0, epi=E_GB, pre=ws.h[j])
-            _lib.call("jg_colsum", ws.gh.data_ptr(), opc, p[b + "tok1.b"].grad.data_ptr(), B * E, K, K)
+                K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tn, E)
+            self._gemm(ws.gh, ws.gx2_op, p[b + "tok2.w"].op, MN, MN, E, Kd, Tn, B, Tn * E, 0, epi=E_GB, pre=ws.h[j])
+            K.colsum(ws.gh, p[b + "tok1.b"].grad, B * E, Kd)
             # tok1 (TN): gu = W1 gh^T ; dW1 += sum_b u gh
-            self._gemm(ws.gu, p[b + "tok1.w"].op, ws.gh, KM, KM, Tn, E, K, B, 0, E * K)
-            self._gemm(p[b + "tok1.w"].grad, ws.u[j], ws.gh, KM, MN, Tn, K, E, B, Tn * E, E * K,
+            self._gemm(ws.gu, p[b + "tok1.w"].op, ws.gh, KM, KM, Tn, E, Kd, B, 0, E * Kd)
+            self._gemm(p[b + "tok1.w"].grad, ws.u[j], ws.gh, KM, MN, Tn, Kd, E, B, Tn * E, E * Kd,
                        reduce_batch=True, epi=E_ACC)
             # ln1 backward + residual: g = g_x2 + LN1'(gu)
             self._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, g, g_op, M, E)
         # encoder (NT): dWenc += g^T xp ; db += sum g (the input gradient is not needed, model.py:444-445)
         self._gemm(p["enc.w"].grad, g_op, ws.xp, MN, MN, E, F, M, epi=E_ACC)
-        _lib.call("jg_colsum", g.data_ptr(), _lib.JG_F32, p["enc.b"].grad.data_ptr(), M, E, E)
+        K.colsum(g, p["enc.b"].grad, M, E)
 
     def _ln_bwd(self, x, gin, pre, mr, bst, resid, out, out_op, rows, cols, c_total=None, row_reduce=None):
+        """Two-phase layer-norm backward + residual add (model.py:242-250): row sums (all-reduced
+        over the row group by `row_reduce` when the normalised axis is split), then apply."""
         p = self.params
         c_total = c_total or cols
-        _lib.call("jg_ln_bwd_moments", x.data_ptr(), gin.data_ptr(), p[pre + "gamma"].data.data_ptr(),
-                  mr.data_ptr(), bst.data_ptr(), rows, cols)
+        K.ln_bwd_moments(x, gin, p[pre + "gamma"].data, mr, bst, rows, cols)
         if row_reduce is not None:
             row_reduce(bst)
-        _lib.call("jg_ln_bwd_apply", x.data_ptr(), gin.data_ptr(), p[pre + "gamma"].data.data_ptr(), mr.data_ptr(),
-                  bst.data_ptr(), resid.data_ptr(), out.data_ptr(), None if out_op is out else out_op.data_ptr(),
-                  p[pre + "gamma"].grad.data_ptr(), p[pre + "beta"].grad.data_ptr(), None, rows, cols, c_total)
+        K.ln_bwd_apply(x, gin, p[pre + "gamma"].data, mr, bst, resid, out, out_op, p[pre + "gamma"].grad,
+                       p[pre + "beta"].grad, rows, cols, c_total)
 
     # grid paths are implemented in jigsaw_grid.py (bound below)
     def _forward_grid(self, ws):

@@ -56,6 +56,7 @@ class MpContext:
         self.row_ranks = [group[self.r * self.C + j] for j in range(self.C)]
         self.col_ranks = [group[i * self.C + self.c] for i in range(self.R)]
         self.row_group = self.col_group = None
+        self.mp_group = None
         if self.n > 1:
             self._build_groups()
 
@@ -65,6 +66,9 @@ class MpContext:
         pg = ProcessGroup(self.comm.world_size, self.n, self.comm.rank)
         for k in range(pg.dp_replicas):
             base = k * self.n
+            g = self.comm.group(list(range(base, base + self.n)))
+            if self.comm.rank in range(base, base + self.n):
+                self.mp_group = g
             for i in range(self.R):
                 ranks = [base + i * self.C + j for j in range(self.C)]
                 g = self.comm.group(ranks) if self.C > 1 else None
@@ -114,6 +118,34 @@ class MpContext:
         out = torch.empty(planes.shape[1:], dtype=planes.dtype, device=planes.device)
         dist.reduce_scatter_tensor(out, planes.contiguous(), group=self.col_group)
         return out
+
+    # -- into pre-allocated outputs (graph-capture friendly; used by the fused model path) --
+    def ag_row_into(self, out: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+        if self.C == 1:
+            out.view(-1).copy_(x.reshape(-1))
+        else:
+            dist.all_gather_into_tensor(out.view(-1), x.reshape(-1), group=self.row_group)
+        return out
+
+    def ag_col_into(self, out: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+        if self.R == 1:
+            out.view(-1).copy_(x.reshape(-1))
+        else:
+            dist.all_gather_into_tensor(out.view(-1), x.reshape(-1), group=self.col_group)
+        return out
+
+    def rs_row_into(self, out: torch.Tensor, planes: torch.Tensor) -> torch.Tensor:
+        dist.reduce_scatter_tensor(out.view(-1), planes.reshape(-1), group=self.row_group)
+        return out
+
+    def rs_col_into(self, out: torch.Tensor, planes: torch.Tensor) -> torch.Tensor:
+        dist.reduce_scatter_tensor(out.view(-1), planes.reshape(-1), group=self.col_group)
+        return out
+
+    def all_reduce_all(self, x: torch.Tensor) -> torch.Tensor:
+        if self.n > 1:
+            dist.all_reduce(x, group=self.mp_group)
+        return x
 
     def all_reduce_row(self, x: torch.Tensor) -> torch.Tensor:
         if self.C > 1:

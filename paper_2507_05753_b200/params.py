@@ -51,24 +51,33 @@ class FlatParams:
 
     CLASSES = ("encdec", "body")
 
+    KINDS = ("matrix", "vec_col", "vec_row")
+
     def __init__(self, specs, device, op_dtype: torch.dtype):
-        # specs: list of (name, local_shape, lr_class, dup_positions) in registration order
+        # specs: list of (name, local_shape, lr_class, dup_positions, kind) in registration order.
+        # Storage order: lr class, then kind, so each (class, kind) is one contiguous range:
+        # Adam runs once per class and the duplicated-vector gradient sync is one all-reduce
+        # per (class, vector kind).
         self.specs = list(specs)
         self.device = device
         self.op_dtype = op_dtype
         self.offsets: dict[str, int] = {}
         self.class_range: dict[str, tuple[int, int]] = {}
+        self.kind_range: dict[tuple[str, str], tuple[int, int]] = {}
         off = 0
         for cls in self.CLASSES:
             start = off
-            for name, shape, lr_class, _ in self.specs:
-                if lr_class != cls:
-                    continue
-                self.offsets[name] = off
-                numel = 1
-                for s in shape:
-                    numel *= s
-                off += -(-numel // ALIGN) * ALIGN
+            for kind in self.KINDS:
+                kstart = off
+                for name, shape, lr_class, _, pkind in self.specs:
+                    if lr_class != cls or pkind != kind:
+                        continue
+                    self.offsets[name] = off
+                    numel = 1
+                    for s in shape:
+                        numel *= s
+                    off += -(-numel // ALIGN) * ALIGN
+                self.kind_range[(cls, kind)] = (kstart, off)
             self.class_range[cls] = (start, off)
         self.total = off
         f32 = dict(dtype=torch.float32, device=device)
@@ -78,7 +87,7 @@ class FlatParams:
         self.v = torch.zeros(self.total, **f32)
         self.op = self.master if op_dtype == torch.float32 else torch.zeros(self.total, dtype=op_dtype, device=device)
         self.params: dict[str, Param] = {}
-        for name, shape, lr_class, dup in self.specs:
+        for name, shape, lr_class, dup, _ in self.specs:
             o = self.offsets[name]
             numel = 1
             for s in shape:

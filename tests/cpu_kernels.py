@@ -1,0 +1,211 @@
+"""TEST DOUBLE (tests only): torch-CPU implementations of paper_2507_05753_b200.kernels.
+
+Lets the gloo multi-process tests run the real host-side Jigsaw schedule (layouts,
+collectives, buffer plumbing in model.py / jigsaw_grid.py) on CPU, with the kernel layer
+swapped for exact float64 arithmetic that follows the C ABI's documented semantics
+(include/jigsaw_sm100.h). Never used by the package; install() monkeypatches it in a test.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+EPI_ACCUM, EPI_BIAS_COL, EPI_BIAS_ROW, EPI_RESID = 1, 2, 4, 8
+EPI_GELU_FWD, EPI_GELU_BWD, EPI_COPY_D2, EPI_STATS = 16, 32, 64, 128
+KM = 0
+
+
+def _view(t, size, stride, extra=0):
+    return torch.as_strided(t, size, stride, t.storage_offset() + extra)
+
+
+def _gelu(x):
+    return x * 0.5 * (1.0 + torch.erf(x / math.sqrt(2.0)))
+
+
+def _gelu_grad(x):
+    return 0.5 * (1.0 + torch.erf(x / math.sqrt(2.0))) + x * torch.exp(-0.5 * x * x) / math.sqrt(2 * math.pi)
+
+
+def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias, bias_bs, resid, ldr, r_bs,
+                    pre, ldp, p_bs, stats, stats_bs):
+    v = v * alpha
+    if epi & EPI_BIAS_COL:
+        v = v + _view(bias, (n,), (1,), ob * bias_bs).double()[None, :]
+    if epi & EPI_BIAS_ROW:
+        v = v + _view(bias, (m,), (1,), ob * bias_bs).double()[:, None]
+    if epi & EPI_RESID:
+        v = v + _view(resid, (m, n), (ldr, 1), ob * r_bs).double()
+    if epi & EPI_GELU_BWD:
+        v = v * _gelu_grad(_view(pre, (m, n), (ldp, 1), ob * p_bs).double())
+    if d is not None:
+        dv = _view(d, (m, n), (ldd, 1), ob * d_bs)
+        if epi & EPI_ACCUM:
+            v = v + dv.double()
+        dv.copy_(v.to(d.dtype))
+    if epi & (EPI_GELU_FWD | EPI_COPY_D2):
+        _view(d2, (m, n), (ldd2, 1), ob * d2_bs).copy_((_gelu(v) if epi & EPI_GELU_FWD else v).to(d2.dtype))
+    if epi & EPI_STATS:
+        sv = _view(stats, (m, 2), (2, 1), ob * stats_bs)
+        sv[:, 0] += v.sum(1).to(sv.dtype)
+        sv[:, 1] += (v * v).sum(1).to(sv.dtype)
+
+
+def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=False, epi=0, alpha=1.0, d2=None,
+         bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
+         d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None):
+    lda = lda if lda is not None else (k if am == KM else m)
+    ldb = ldb if ldb is not None else (k if bm == KM else n)
+    ldd = ldd if ldd is not None else n
+    d_bs = d_bs if d_bs is not None else (0 if reduce_batch else m * n)
+    d2_bs = d2_bs if d2_bs is not None else (0 if reduce_batch else m * n)
+    r_bs = r_bs if r_bs else m * n
+    p_bs = p_bs if p_bs else m * n
+    stats_bs = stats_bs if stats_bs else 2 * m
+    acc = []
+    for bi in range(batch):
+        A = _view(a, (m, k), (lda, 1) if am == KM else (1, lda), bi * a_bs).double()
+        B = _view(b, (n, k), (ldb, 1) if bm == KM else (1, ldb), bi * b_bs).double()
+        acc.append(A @ B.T)
+    if reduce_batch:
+        acc = [sum(acc)]
+    for ob, v in enumerate(acc):
+        _apply_epilogue(v, ob, m, n, epi, alpha, out, ldd, d_bs, d2, n, d2_bs, bias, bias_bs, resid, n, r_bs,
+                        pre, n, p_bs, stats, stats_bs)
+    return out
+
+
+def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0, d2=None,
+             ldd2=None, d2_bs=0, bias=None, bias_bs=0, resid=None, ldr=None, r_bs=0, pre=None, ldp=None, p_bs=0,
+             stats=None, stats_bs=0):
+    acc_ld = acc_ld if acc_ld is not None else n
+    for ob in range(batch):
+        v = _view(acc, (m, n), (acc_ld, 1), ob * acc_bs).double()
+        _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd if ldd is not None else n, d_bs, d2,
+                        ldd2 if ldd2 is not None else n, d2_bs, bias, bias_bs, resid, ldr if ldr is not None else n,
+                        r_bs, pre, ldp if ldp is not None else n, p_bs, stats, stats_bs)
+
+
+def axpy(y, x, alpha=1.0):
+    y.add_(x.reshape(y.shape), alpha=alpha)
+
+
+def cast_bf16(x, y):
+    y.copy_(x.to(y.dtype))
+
+
+def patchify(x, tok, batch, lat, lon, chans, pl, pw):
+    t = x.reshape(batch, lat // pl, pl, lon // pw, pw, chans).permute(0, 1, 3, 5, 2, 4)
+    tok.copy_(t.reshape(tok.shape).to(tok.dtype))
+
+
+def _unpatchify(tok, batch, lat, lon, chans, pl, pw):
+    t = tok.reshape(batch, lat // pl, lon // pw, chans, pl, pw).permute(0, 1, 4, 2, 5, 3)
+    return t.reshape(batch, lat, lon, chans)
+
+
+def ln_moments(x, stats, rows, cols):
+    xv = x.reshape(rows, cols).double()
+    stats.view(rows, 2)[:, 0] += xv.sum(1).float()
+    stats.view(rows, 2)[:, 1] += (xv * xv).sum(1).float()
+
+
+def ln_apply(x, stats, gamma, beta, y, mean_rstd, rows, cols, c_total, eps):
+    st = stats.reshape(rows, 2).double()
+    mean = st[:, 0] / c_total
+    var = st[:, 1] / c_total - mean * mean
+    rstd = 1.0 / torch.sqrt(var + eps)
+    if mean_rstd is not None:
+        mean_rstd.reshape(rows, 2).copy_(torch.stack([mean, rstd], 1).float())
+    xv = x.reshape(rows, cols).double()
+    y.reshape(rows, cols).copy_((gamma.double() * (xv - mean[:, None]) * rstd[:, None] + beta.double()).to(y.dtype))
+
+
+def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
+    mr = mean_rstd.reshape(rows, 2).double()
+    xh = (x.reshape(rows, cols).double() - mr[:, :1]) * mr[:, 1:]
+    h = g.reshape(rows, cols).double() * gamma.double()
+    bs = bstats.reshape(rows, 2)
+    bs[:, 0] += h.sum(1).float()
+    bs[:, 1] += (h * xh).sum(1).float()
+
+
+def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total):
+    mr = mean_rstd.reshape(rows, 2).double()
+    xh = (x.reshape(rows, cols).double() - mr[:, :1]) * mr[:, 1:]
+    gv = g.reshape(rows, cols).double()
+    h = gv * gamma.double()
+    bs = bstats.reshape(rows, 2).double()
+    dx = mr[:, 1:] * (h - bs[:, :1] / c_total - xh * bs[:, 1:] / c_total)
+    if resid is not None:
+        dx = dx + resid.reshape(rows, cols).double()
+    out.reshape(rows, cols).copy_(dx.to(out.dtype))
+    if out_op is not None and out_op is not out:
+        out_op.reshape(rows, cols).copy_(dx.to(out_op.dtype))
+    if dgamma is not None:
+        dgamma += (gv * xh).sum(0).float()
+    if dbeta is not None:
+        dbeta += gv.sum(0).float()
+
+
+def colsum(x, out, rows, cols, ld=None):
+    out += _view(x, (rows, cols), (ld or cols, 1)).double().sum(0).float()
+
+
+def rowsum(x, out, rows, cols, ld=None):
+    out += _view(x, (rows, cols), (ld or cols, 1)).double().sum(1).float()
+
+
+def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blend, g_dec, batch, lat, lon, chans,
+               pl, pw, inv_count, loss_scale):
+    decoded = _unpatchify(dec.double(), batch, lat, lon, chans, pl, pw)
+    x = xin.double()
+    w = blend_w.double()
+    o = w * decoded + (1 - w) * x
+    if out is not None:
+        out.copy_(o.float())
+    if g_ext is None and target is None:
+        return
+    if g_ext is not None:
+        gout = g_ext.double()
+    else:
+        wt = lat_w.double()[None, :, None, None] * var_w.double()[None, None, None, :]
+        e = o - target.double()
+        if loss is not None:
+            loss += float((wt * e * e).sum() * inv_count)
+        gout = 2 * wt * e * inv_count * loss_scale
+    if g_blend is not None:
+        g_blend += (gout * (decoded - x)).sum((0, 1, 2)).float()
+    if g_dec is not None:
+        gd = gout * w
+        t = gd.reshape(batch, lat // pl, pl, lon // pw, pw, chans).permute(0, 1, 3, 5, 2, 4)
+        g_dec.copy_(t.reshape(g_dec.shape).to(g_dec.dtype))
+
+
+def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None):
+    t = int(step.item())
+    pv, gv, mv, vv = p[:n], g[:n], m[:n], v[:n]
+    s = float(grad_scale.item()) if grad_scale is not None else 1.0
+    gg = gv * s
+    mv.mul_(beta1).add_((1 - beta1) * gg)
+    vv.mul_(beta2).add_((1 - beta2) * gg * gg)
+    pv.sub_(lr * (mv / (1 - beta1 ** t)) / (torch.sqrt(vv / (1 - beta2 ** t)) + eps))
+    if p_op is not None:
+        p_op[:n].copy_(pv.to(p_op.dtype))
+
+
+def step_increment(counter):
+    counter += 1
+
+
+NAMES = ["gemm", "epilogue", "axpy", "cast_bf16", "patchify", "ln_moments", "ln_apply", "ln_bwd_moments",
+         "ln_bwd_apply", "colsum", "rowsum", "blend_loss", "adam", "step_increment"]
+
+
+def install():
+    """Swap the package's kernel layer for this double (call inside a test process only)."""
+    import paper_2507_05753_b200.kernels as K
+    mod = globals()
+    for name in NAMES:
+        setattr(K, name, mod[name])

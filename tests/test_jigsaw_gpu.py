@@ -1,0 +1,29 @@
+"""Jigsaw-sharded GPU runs (NCCL, one process per GPU) agree with the reference and with the
+single-GPU tolerances: 1e-4 (f32 / 3xTF32) and 2e-2 (bf16). Needs >= 2 GPUs on the box."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_jigsaw_nccl_parity(n):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29561", os.path.join(HERE, "mp_check.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    line = [ln for ln in p.stdout.splitlines() if ln.startswith("MPCHECK ")]
+    assert p.returncode == 0 and line, p.stdout[-3000:] + p.stderr[-3000:]
+    res = json.loads(line[0][len("MPCHECK "):])
+    print(res)
+    for key, tol in (("G1_f32", 1e-4), ("C2_f32", 1e-4), ("G1_bf16", 2e-2), ("C2_bf16", 2e-2)):
+        assert res[key]["out"] < tol and res[key]["grad"] < tol, (key, res[key])
