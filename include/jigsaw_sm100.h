@@ -51,6 +51,9 @@ extern "C" {
 #define JG_EPI_GELU_BWD 32u /* result *= gelu'(pre[row,col])                   (tensor.py:80-84)   */
 #define JG_EPI_COPY_D2 64u  /* D2 = result as well (e.g. bf16 operand copy of an fp32 output)     */
 #define JG_EPI_STATS 128u   /* stats[row] += (sum_col result, sum_col result^2)  (model.py:234)     */
+#define JG_EPI_ADAM 256u    /* result is a complete weight gradient: apply Adam to D = fp32 master
+                               in place (m, v, bf16 copy alongside) instead of storing the gradient
+                               (fused into the producer; no gradient round trip) */
 
 /*
  * jg_gemm — one (batched) GEMM with a fused epilogue.
@@ -84,6 +87,10 @@ typedef struct jg_gemm_desc {
   const float* resid; int64_t ldr, r_bstride;
   const void* pre; int64_t ldp, p_bstride; int32_t pre_type;
   float* stats; int64_t stats_bstride;   /* [rows][2] fp32, must be zeroed by the caller */
+  /* JG_EPI_ADAM: moments with D's indexing (ld = ldd, batch stride = d_bstride), optional bf16
+   * copy of the updated weight (same indexing), step counter t >= 1 on the device. */
+  float* adam_m; float* adam_v; void* adam_pbf16; const int32_t* adam_step;
+  float adam_lr, adam_beta1, adam_beta2, adam_eps;
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);

@@ -27,6 +27,7 @@ JG_KMAJOR, JG_MNMAJOR = 0, 1
 JG_MATH_BF16, JG_MATH_TF32X3 = 0, 1
 EPI_ACCUM, EPI_BIAS_COL, EPI_BIAS_ROW, EPI_RESID = 1, 2, 4, 8
 EPI_GELU_FWD, EPI_GELU_BWD, EPI_COPY_D2, EPI_STATS = 16, 32, 64, 128
+EPI_ADAM = 256
 
 EXPORTED = [
     "jg_gemm", "jg_split_tf32", "jg_split_tf32_2d", "jg_cast_bf16", "jg_gelu_fwd", "jg_gelu_bwd",
@@ -52,6 +53,9 @@ class GemmDesc(ctypes.Structure):
         ("resid", ctypes.c_void_p), ("ldr", ctypes.c_int64), ("r_bstride", ctypes.c_int64),
         ("pre", ctypes.c_void_p), ("ldp", ctypes.c_int64), ("p_bstride", ctypes.c_int64), ("pre_type", ctypes.c_int32),
         ("stats", ctypes.c_void_p), ("stats_bstride", ctypes.c_int64),
+        ("adam_m", ctypes.c_void_p), ("adam_v", ctypes.c_void_p), ("adam_pbf16", ctypes.c_void_p),
+        ("adam_step", ctypes.c_void_p), ("adam_lr", ctypes.c_float), ("adam_beta1", ctypes.c_float),
+        ("adam_beta2", ctypes.c_float), ("adam_eps", ctypes.c_float),
     ]
 
 

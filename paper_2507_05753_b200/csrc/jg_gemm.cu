@@ -48,6 +48,8 @@ struct GemmParams {
   const float* resid; int64_t ldr, r_bs;
   const void* pre; int64_t ldp, p_bs; int pre_bf16;
   float* stats; int64_t stats_bs;
+  float* adam_m; float* adam_v; __nv_bfloat16* adam_pbf16; const int32_t* adam_step;
+  float adam_lr, adam_b1, adam_b2, adam_eps;
 };
 
 template <int BN, bool TF32>
@@ -279,6 +281,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             s2 += x * x;
           }
         }
+        if (epi & JG_EPI_ADAM) {
+          // v[] is the complete gradient of this weight tile: update D (= master) in place
+          const float* mp = p.adam_m;
+          const int t = *p.adam_step;
+          const float bc1 = 1.0f / (1.0f - powf(p.adam_b1, (float)t));
+          const float bc2 = 1.0f / (1.0f - powf(p.adam_b2, (float)t));
+          float* dp = reinterpret_cast<float*>(p.d);
+          (void)mp;
+          if (full_chunk) {
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+              float w[8], mm[8], vv[8];
+              const int64_t o = drow + col0 + g8 * 8;
+              jgd::load8(dp, o, false, w);
+              jgd::load8(p.adam_m, o, false, mm);
+              jgd::load8(p.adam_v, o, false, vv);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float gj = v[g8 * 8 + j];
+                mm[j] = p.adam_b1 * mm[j] + (1.0f - p.adam_b1) * gj;
+                vv[j] = p.adam_b2 * vv[j] + (1.0f - p.adam_b2) * gj * gj;
+                w[j] -= p.adam_lr * (mm[j] * bc1) / (sqrtf(vv[j] * bc2) + p.adam_eps);
+              }
+              jgd::store8(dp, o, false, w);
+              jgd::store8(p.adam_m, o, false, mm);
+              jgd::store8(p.adam_v, o, false, vv);
+              if (p.adam_pbf16) jgd::store8(p.adam_pbf16, o, true, w);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < ncol) {
+                const int64_t o = drow + col0 + j;
+                const float gj = v[j];
+                const float mm = p.adam_b1 * p.adam_m[o] + (1.0f - p.adam_b1) * gj;
+                const float vv = p.adam_b2 * p.adam_v[o] + (1.0f - p.adam_b2) * gj * gj;
+                const float w = dp[o] - p.adam_lr * (mm * bc1) / (sqrtf(vv * bc2) + p.adam_eps);
+                dp[o] = w;
+                p.adam_m[o] = mm;
+                p.adam_v[o] = vv;
+                if (p.adam_pbf16) p.adam_pbf16[o] = __float2bfloat16_rn(w);
+              }
+            }
+          }
+          continue;
+        }
         // primary output
         if (p.d != nullptr) {
           if (full_chunk) {
@@ -433,6 +481,10 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   JG_SHAPE_CHECK(!(epi & JG_EPI_RESID) || (g->resid && out_ok(g->resid, g->ldr, JG_F32)), "jg_gemm: bad resid");
   JG_SHAPE_CHECK(!(epi & JG_EPI_GELU_BWD) || (g->pre && out_ok(g->pre, g->ldp, g->pre_type)), "jg_gemm: bad pre");
   JG_SHAPE_CHECK(!(epi & JG_EPI_STATS) || g->stats, "jg_gemm: STATS without stats buffer");
+  JG_SHAPE_CHECK(!(epi & JG_EPI_ADAM) || (g->d && g->d_type == JG_F32 && g->adam_m && g->adam_v && g->adam_step &&
+                                          aligned16(g->adam_m) && aligned16(g->adam_v) &&
+                                          !(epi & (JG_EPI_ACCUM | JG_EPI_GELU_FWD | JG_EPI_COPY_D2 | JG_EPI_STATS))),
+                 "jg_gemm: ADAM needs fp32 D (the master weights), aligned m/v, a step counter, and no other outputs");
 
   GemmParams p;
   memset(&p, 0, sizeof(p));
@@ -484,6 +536,9 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   p.resid = g->resid; p.ldr = g->ldr; p.r_bs = g->r_bstride;
   p.pre = g->pre; p.ldp = g->ldp; p.p_bs = g->p_bstride; p.pre_bf16 = g->pre_type == JG_BF16;
   p.stats = g->stats; p.stats_bs = g->stats_bstride;
+  p.adam_m = g->adam_m; p.adam_v = g->adam_v; p.adam_pbf16 = static_cast<__nv_bfloat16*>(g->adam_pbf16);
+  p.adam_step = g->adam_step; p.adam_lr = g->adam_lr; p.adam_b1 = g->adam_beta1; p.adam_b2 = g->adam_beta2;
+  p.adam_eps = g->adam_eps;
 
   if (tf32) {
     if (bn == 256) return launch<256, true>(p, stream);

@@ -22,8 +22,11 @@ from .train import AdamConfig
 
 class TrainStep:
     def __init__(self, model: WeatherMixerModel, batch: int = 1, r: int = 1, adam: AdamConfig | None = None,
-                 graph: bool = True, loss_scale: float = 1.0):
+                 graph: bool = True, loss_scale: float = 1.0, fused_adam: bool = True):
         self.model, self.batch, self.r = model, batch, r
+        # Adam fused into the weight-gradient GEMM epilogues: valid when every weight receives
+        # exactly one gradient GEMM per step (rollout 1; one sample per GEMM on the grid path).
+        self.fused_adam = fused_adam and r == 1 and (model.ctx.n == 1 or batch == 1)
         self.adam = adam or AdamConfig()
         self.loss_scale = loss_scale
         self.ws = model.workspace(batch, r)
@@ -33,28 +36,39 @@ class TrainStep:
         self.use_graph = graph
         self.graph = None
         self.launches_per_step = None
-        self._pinned_loss = torch.zeros(1, dtype=torch.float32, pin_memory=True)
+        self._pinned_loss = torch.zeros(1, dtype=torch.float32, pin_memory=dev.type == "cuda")
         self._h2d_bytes = 2 * self.ws.xin.numel() * 4
         self._d2h_bytes = 4
 
     # -- the step body --------------------------------------------------------------------
     def _body(self) -> None:
-        m, ws = self.model, self.ws
-        m.zero_grads()
+        m, ws, f = self.model, self.ws, self.model.flat
+        K.step_increment(self.step_count)
+        if self.fused_adam:
+            for cls in f.CLASSES:  # matrix gradients never hit HBM; only vector grads accumulate
+                lo, hi = f.vec_range(cls)
+                f.grad[lo:hi].zero_()
+        else:
+            m.zero_grads()
         m._forward(ws)
         ws.loss.zero_()
         m._blend(ws, target=self.target, loss=ws.loss, loss_scale=self.loss_scale)
         if m.ctx.n > 1:
             m.ctx.all_reduce_all(ws.loss)  # the loss is a sum of per-tile terms
-        m._backward(ws)
+        m._fused_adam = (self.step_count, self.adam) if self.fused_adam else None
+        try:
+            m._backward(ws)
+        finally:
+            m._fused_adam = None
         m.grad_sync()
         self._adam()
 
     def _adam(self) -> None:
         f, a = self.model.flat, self.adam
-        K.step_increment(self.step_count)
         op_copy = f.op if f.op is not f.master else None
         for cls, (lo, hi) in f.class_range.items():
+            if self.fused_adam:
+                lo, hi = f.vec_range(cls)
             if hi <= lo:
                 continue
             K.adam(f.master[lo:], f.grad[lo:], f.m[lo:], f.v[lo:], None if op_copy is None else op_copy[lo:],

@@ -112,15 +112,15 @@ def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None
     m.ctx.ag_row_into(dyrow, dY)
     if dX is not None:
         K.gemm(dX, dyrow, panel, KM, MN, M, kin_l, nl, C, M * nl, nl * kin_l, reduce_batch=True, **dx_epi)
-    wgrad = m.params[wname].grad
     if R == 1:
-        K.gemm(wgrad, dyrow, X, MN, MN, nl, kin_l, M, C, M * nl, 0, d_bs=nl * kin_l, epi=E_ACC)
+        out, kw = m._wgrad(wname)
+        K.gemm(out, dyrow, X, MN, MN, nl, kin_l, M, C, M * nl, 0, d_bs=nl * kin_l, **kw)
     else:
         P = g.scratch[:nout * kin_l].view(C, nl, kin_l)
         K.gemm(P, dyrow, X, MN, MN, nl, kin_l, M, C, M * nl, 0, d_bs=nl * kin_l)
         red = g.red[:(nout // R) * kin_l].view(nout // R, kin_l)
         m.ctx.rs_col_into(red, P.view(R, nout // R, kin_l))
-        K.axpy(wgrad, red)
+        m._wgrad_reduced(wname, red)
     K.colsum(bias_src, m.params[bname].grad, M, nl)
 
 
@@ -215,9 +215,6 @@ def backward_grid(m, ws) -> None:
             grow = g.op_scratch2[:C * Tl * El].view(C, Tl, El)
             ctx.ag_row_into(grow, ws.gx2_op[bi])
             acol = g.a_col[j][bi] if R > 1 else ws.a[j][bi]
-            K.gemm(p[b + "tok2.w"].grad, grow, acol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True,
-                   epi=E_ACC)
-            K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
             if R == 1:
                 K.gemm(ws.gh[bi], grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
                        epi=E_GB, pre=ws.h[j][bi])
@@ -227,6 +224,12 @@ def backward_grid(m, ws) -> None:
                 red = g.red[:Er * Kl].view(Er, Kl)
                 ctx.rs_col_into(red, P.view(R, Er, Kl))
                 K.epilogue(red, Er, Kl, epi=E_GB, pre=ws.h[j][bi], d=ws.gh[bi])
+            K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
+            if B == 1:
+                out, kw = m._wgrad(b + "tok2.w")
+            else:  # several samples accumulate: only the plain gradient sink can sum them
+                out, kw = p[b + "tok2.w"].grad, {"epi": E_ACC}
+            K.gemm(out, grow, acol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
         K.colsum(ws.gh, p[b + "tok1.b"].grad, B * Er, Kl)
         for bi in range(B):
             # tok1 backward: gu = W1 gh^T (RS over the row group) ; dW1 += sum_e u gh
@@ -238,8 +241,11 @@ def backward_grid(m, ws) -> None:
             P = g.scratch[:C * Tl * El].view(C, Tl, El)
             K.gemm(P, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=Tl * El)
             ctx.rs_row_into(ws.gu[bi], P)
-            K.gemm(p[b + "tok1.w"].grad, g.u_row[j][bi], ghcol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl,
-                   reduce_batch=True, epi=E_ACC)
+            if B == 1:
+                out, kw = m._wgrad(b + "tok1.w")
+            else:
+                out, kw = p[b + "tok1.w"].grad, {"epi": E_ACC}
+            K.gemm(out, g.u_row[j][bi], ghcol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
         m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, gop, M, El, E,
                   row_reduce=ctx.all_reduce_row)
     # encoder: dW only (the input gradient is not needed, model.py:444-445)

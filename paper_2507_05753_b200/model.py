@@ -396,6 +396,37 @@ class WeatherMixerModel:
                      bw.grad if want_grad else None, ws.gd if want_grad else None, ws.B, lat, lon, self.local_vars,
                      cfg.patch[0], cfg.patch[1], ws.inv_count, loss_scale)
 
+    # -- weight-gradient sink ---------------------------------------------------------------
+    def _wgrad(self, name):
+        """(out, epilogue kwargs) for the GEMM producing weight `name`'s complete gradient.
+
+        Normally the gradient accumulates into Param.grad (reference add_grad, parallel.py:490-493).
+        Inside TrainStep with fused Adam (rollout 1: each weight gets exactly one gradient GEMM)
+        the GEMM epilogue applies Adam to the master weight directly (JG_EPI_ADAM) and the
+        gradient never touches HBM; the caller orders every dX GEMM before its dW GEMM.
+        """
+        p = self.params[name]
+        fa = getattr(self, "_fused_adam", None)
+        if fa is None:
+            return p.grad, {"epi": E_ACC}
+        step, cfg = fa
+        f = self.flat
+        return p.data, {"epi": _lib.EPI_ADAM, "adam": (f.view(name, f.m), f.view(name, f.v),
+                                                      None if f.op is f.master else p.op, step, cfg.lr(p.lr_class),
+                                                      cfg.beta1, cfg.beta2, cfg.eps)}
+
+    def _wgrad_reduced(self, name, red):
+        """Sink for a weight gradient that arrived reduced (NCCL reduce-scatter) in `red`."""
+        p = self.params[name]
+        fa = getattr(self, "_fused_adam", None)
+        if fa is None:
+            K.axpy(p.grad, red)
+            return
+        step, cfg = fa
+        f = self.flat
+        K.adam(p.data, red, f.view(name, f.m), f.view(name, f.v), None if f.op is f.master else p.op,
+               p.data.numel(), cfg.lr(p.lr_class), cfg.beta1, cfg.beta2, cfg.eps, step)
+
     def _backward(self, ws: "_Workspace") -> None:
         if self.ctx.n > 1:
             return self._backward_grid(ws)
@@ -403,40 +434,44 @@ class WeatherMixerModel:
         Tn, E, F, Kd, H = cfg.tokens, cfg.d_emb, cfg.patch_features, cfg.d_tok, cfg.d_ch
         M = B * Tn
         ws.bstats.zero_()
-        # decoder (NT): dW += gd^T y ; db += sum gd ; g = gd Wdec
-        self._gemm(p["dec.w"].grad, ws.gd, ws.y_op, MN, MN, F, E, M, epi=E_ACC)
-        K.colsum(ws.gd, p["dec.b"].grad, M, F)
+        # decoder (NT): g = gd Wdec ; dW += gd^T y ; db += sum gd
         g, g_op = ws.g, ws.g_op
         self._gemm(g, ws.gd, p["dec.w"].op, KM, MN, M, E, F, epi=0 if g_op is g else E_CP,
                    d2=None if g_op is g else g_op)
+        out, kw = self._wgrad("dec.w")
+        self._gemm(out, ws.gd, ws.y_op, MN, MN, F, E, M, **kw)
+        K.colsum(ws.gd, p["dec.b"].grad, M, F)
         nj = ws.r * cfg.n_blocks
         for j in reversed(range(nj)):
             b = f"block{j % cfg.n_blocks}."
-            # ch2: dWc2 += g^T ca ; dbc2 += sum g ; gc = (g Wc2) * gelu'(c)
-            self._gemm(p[b + "ch2.w"].grad, g_op, ws.ca[j], MN, MN, E, H, M, epi=E_ACC)
-            K.colsum(g, p[b + "ch2.b"].grad, M, E)
+            # ch2: gc = (g Wc2) * gelu'(c) ; dWc2 += g^T ca ; dbc2 += sum g
             self._gemm(ws.gc, g_op, p[b + "ch2.w"].op, KM, MN, M, H, E, epi=E_GB, pre=ws.c[j])
-            # ch1: dWc1 += gc^T v ; dbc1 += sum gc ; gv = gc Wc1
-            self._gemm(p[b + "ch1.w"].grad, ws.gc, ws.v[j], MN, MN, H, E, M, epi=E_ACC)
-            K.colsum(ws.gc, p[b + "ch1.b"].grad, M, H)
+            out, kw = self._wgrad(b + "ch2.w")
+            self._gemm(out, g_op, ws.ca[j], MN, MN, E, H, M, **kw)
+            K.colsum(g, p[b + "ch2.b"].grad, M, E)
+            # ch1: gv = gc Wc1 ; dWc1 += gc^T v ; dbc1 += sum gc
             self._gemm(ws.gv, ws.gc, p[b + "ch1.w"].op, KM, MN, M, E, H)
+            out, kw = self._wgrad(b + "ch1.w")
+            self._gemm(out, ws.gc, ws.v[j], MN, MN, H, E, M, **kw)
+            K.colsum(ws.gc, p[b + "ch1.b"].grad, M, H)
             # ln2 backward + residual: g_x2 = g + LN2'(gv)
             self._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], g, ws.gx2, ws.gx2_op, M, E)
-            # tok2 (weight-first): dW2 += sum_b g_x2 a ; db2 += row sums ; gh = (g_x2^T W2) * gelu'(h)
-            self._gemm(p[b + "tok2.w"].grad, ws.gx2_op, ws.a[j], KM, MN, Tn, Kd, E, B, Tn * E, E * Kd,
-                       reduce_batch=True, epi=E_ACC)
+            # tok2 (weight-first): gh = (g_x2^T W2) * gelu'(h) ; dW2 += sum_b g_x2 a ; db2 += row sums
+            self._gemm(ws.gh, ws.gx2_op, p[b + "tok2.w"].op, MN, MN, E, Kd, Tn, B, Tn * E, 0, epi=E_GB, pre=ws.h[j])
+            out, kw = self._wgrad(b + "tok2.w")
+            self._gemm(out, ws.gx2_op, ws.a[j], KM, MN, Tn, Kd, E, B, Tn * E, E * Kd, reduce_batch=True, **kw)
             for bi in range(B):
                 K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tn, E)
-            self._gemm(ws.gh, ws.gx2_op, p[b + "tok2.w"].op, MN, MN, E, Kd, Tn, B, Tn * E, 0, epi=E_GB, pre=ws.h[j])
             K.colsum(ws.gh, p[b + "tok1.b"].grad, B * E, Kd)
             # tok1 (TN): gu = W1 gh^T ; dW1 += sum_b u gh
             self._gemm(ws.gu, p[b + "tok1.w"].op, ws.gh, KM, KM, Tn, E, Kd, B, 0, E * Kd)
-            self._gemm(p[b + "tok1.w"].grad, ws.u[j], ws.gh, KM, MN, Tn, Kd, E, B, Tn * E, E * Kd,
-                       reduce_batch=True, epi=E_ACC)
+            out, kw = self._wgrad(b + "tok1.w")
+            self._gemm(out, ws.u[j], ws.gh, KM, MN, Tn, Kd, E, B, Tn * E, E * Kd, reduce_batch=True, **kw)
             # ln1 backward + residual: g = g_x2 + LN1'(gu)
             self._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, g, g_op, M, E)
         # encoder (NT): dWenc += g^T xp ; db += sum g (the input gradient is not needed, model.py:444-445)
-        self._gemm(p["enc.w"].grad, g_op, ws.xp, MN, MN, E, F, M, epi=E_ACC)
+        out, kw = self._wgrad("enc.w")
+        self._gemm(out, g_op, ws.xp, MN, MN, E, F, M, **kw)
         K.colsum(g, p["enc.b"].grad, M, E)
 
     def _ln_bwd(self, x, gin, pre, mr, bst, resid, out, out_op, rows, cols, c_total=None, row_reduce=None):

@@ -100,5 +100,15 @@ class FlatParams:
     def zero_grads(self) -> None:
         self.grad.zero_()
 
+    def view(self, name: str, buf: torch.Tensor) -> torch.Tensor:
+        """`name`'s view into another flat buffer (m, v, ...) with the same layout."""
+        p = self.params[name]
+        o = self.offsets[name]
+        return buf[o:o + p.data.numel()].view(p.data.shape)
+
+    def vec_range(self, cls: str) -> tuple[int, int]:
+        """Contiguous range of all vector parameters (column then row) of one lr class."""
+        return self.kind_range[(cls, "vec_col")][0], self.kind_range[(cls, "vec_row")][1]
+
     def numel(self) -> int:
         return sum(p.data.numel() for p in self.params.values())

@@ -13,6 +13,7 @@ import torch
 
 EPI_ACCUM, EPI_BIAS_COL, EPI_BIAS_ROW, EPI_RESID = 1, 2, 4, 8
 EPI_GELU_FWD, EPI_GELU_BWD, EPI_COPY_D2, EPI_STATS = 16, 32, 64, 128
+EPI_ADAM = 256
 KM = 0
 
 
@@ -54,7 +55,7 @@ def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias
 
 def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=False, epi=0, alpha=1.0, d2=None,
          bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
-         d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None):
+         d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None):
     lda = lda if lda is not None else (k if am == KM else m)
     ldb = ldb if ldb is not None else (k if bm == KM else n)
     ldd = ldd if ldd is not None else n
@@ -70,6 +71,20 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
         acc.append(A @ B.T)
     if reduce_batch:
         acc = [sum(acc)]
+    if epi & EPI_ADAM:
+        am_, av_, apb, astep, lr, b1, b2, eps = adam
+        t = int(astep.item())
+        for ob, v in enumerate(acc):
+            w = _view(out, (m, n), (ldd, 1), ob * d_bs)
+            mm = _view(am_, (m, n), (ldd, 1), ob * d_bs)
+            vv = _view(av_, (m, n), (ldd, 1), ob * d_bs)
+            gg = (v * alpha).float()
+            mm.mul_(b1).add_((1 - b1) * gg)
+            vv.mul_(b2).add_((1 - b2) * gg * gg)
+            w.sub_(lr * (mm / (1 - b1 ** t)) / (torch.sqrt(vv / (1 - b2 ** t)) + eps))
+            if apb is not None:
+                _view(apb, (m, n), (ldd, 1), ob * d_bs).copy_(w.to(apb.dtype))
+        return out
     for ob, v in enumerate(acc):
         _apply_epilogue(v, ob, m, n, epi, alpha, out, ldd, d_bs, d2, n, d2_bs, bias, bias_bs, resid, n, r_bs,
                         pre, n, p_bs, stats, stats_bs)
@@ -185,14 +200,14 @@ def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blen
 
 def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None):
     t = int(step.item())
-    pv, gv, mv, vv = p[:n], g[:n], m[:n], v[:n]
+    pv, gv, mv, vv = p.reshape(-1)[:n], g.reshape(-1)[:n], m.reshape(-1)[:n], v.reshape(-1)[:n]
     s = float(grad_scale.item()) if grad_scale is not None else 1.0
     gg = gv * s
     mv.mul_(beta1).add_((1 - beta1) * gg)
     vv.mul_(beta2).add_((1 - beta2) * gg * gg)
     pv.sub_(lr * (mv / (1 - beta1 ** t)) / (torch.sqrt(vv / (1 - beta2 ** t)) + eps))
     if p_op is not None:
-        p_op[:n].copy_(pv.to(p_op.dtype))
+        p_op.reshape(-1)[:n].copy_(pv.to(p_op.dtype))
 
 
 def step_increment(counter):

@@ -1,0 +1,167 @@
+"""Host-side API parity on CPU: layout API (reference test_sharding.py), config validation and
+hashing (model.py:73-111), process groups (test_comm.py:214-236), parameter layouts
+(model.py:124-197) and the analytic communication volume (parallel.py:361-466)."""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import model as om
+from paper_2507_05753_b200 import ConfigError, ModelConfig, ProcessGroup, ShardSpec, gather, shard
+from paper_2507_05753_b200.config import token_sets
+from paper_2507_05753_b200.model import Layout
+from paper_2507_05753_b200.parallel import comm_volume, primitive_send_elements
+from paper_2507_05753_b200.sharding import contiguous_split, pad_axes, padded_size
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ sharding (test_sharding.py)
+def test_two_way_placement_and_round_trip(rng):
+    x = rng.standard_normal((3, 5, 7))
+    specs = [ShardSpec(2, r, x.shape) for r in range(2)]
+    blocks = [shard(x, s) for s in specs]
+    assert blocks[0].shape == (3, 5, 4) and specs[1].pad_cols == 1
+    assert np.array_equal(blocks[1][..., -1], np.zeros((3, 5)))  # high-side zero padding
+    assert np.array_equal(gather(blocks, specs), x)
+
+
+def test_four_and_eight_way_round_trip_numpy_and_torch(rng):
+    for n in (4, 8):
+        x = rng.standard_normal((2, 9, 6))
+        specs = [ShardSpec(n, r, x.shape) for r in range(n)]
+        blocks = [shard(x, s) for s in specs]
+        assert np.array_equal(gather(blocks, specs), x)
+        xt = torch.tensor(x)
+        tb = [shard(xt, s) for s in specs]
+        assert torch.equal(gather(tb, specs), xt)
+    s = ShardSpec(4, 3, (6, 8))
+    assert (s.block_row, s.block_col, s.local_shape) == (1, 1, (3, 4))
+
+
+def test_shard_errors():
+    with pytest.raises(ValueError):
+        ShardSpec(3, 0, (4, 4))
+    with pytest.raises(ValueError):
+        ShardSpec(2, 2, (4, 4))
+    with pytest.raises(ValueError):
+        ShardSpec(4, 0, (4,))
+    with pytest.raises(ValueError):
+        gather([np.zeros((2, 2))], [ShardSpec(2, 0, (2, 4))])
+    with pytest.raises(ValueError):
+        pad_axes(np.zeros(4), {0: 2})
+    assert padded_size(7, 2) == 8
+    assert [list(c) for c in contiguous_split(5, 2)] == [[0, 1, 2], [3, 4, 5]]
+
+
+def test_custom_strided_split_round_trip(rng):
+    x = rng.standard_normal((4, 8))
+    split = (np.array([0, 2, 4, 6]), np.array([1, 3, 5, 7]))
+    specs = [ShardSpec(2, r, x.shape, col_split=split) for r in range(2)]
+    blocks = [shard(x, s) for s in specs]
+    assert np.array_equal(blocks[1], x[:, 1::2])
+    assert np.array_equal(gather(blocks, specs), x)
+
+
+# ------------------------------------------------------------------ config (model.py:41-111)
+def test_validate_rules():
+    ModelConfig().validate(1)
+    with pytest.raises(ConfigError, match="n_vars"):
+        ModelConfig(n_vars=7).validate(2)
+    with pytest.raises(ConfigError, match="longitude patches"):
+        ModelConfig(grid=(32, 60), patch=(4, 4)).validate(4)  # 15 lon patches
+    with pytest.raises(ConfigError, match="not divisible"):
+        ModelConfig(grid=(30, 64)).validate(1)
+    with pytest.raises(ConfigError):
+        ModelConfig(d_emb=0).validate(1)
+    ModelConfig(grid=(32, 64), patch=(4, 4)).validate(8)  # 16 lon patches / 4
+    c4 = ModelConfig(n_vars=70, grid=(728, 1440), patch=(8, 8), d_emb=4320, d_tok=8640, d_ch=4320, n_blocks=3)
+    for n in (1, 2, 4, 8):
+        c4.validate(n)
+    assert abs(c4.train_flops() / 1e9 - 36818.7) < 0.1  # GFLOP per sample, BASELINE.md C4
+
+
+def test_content_hash_matches_reference_algorithm():
+    import hashlib
+    c = ModelConfig()
+    expect = hashlib.sha256(json.dumps(c.to_dict(), sort_keys=True).encode()).hexdigest()[:16]
+    assert c.content_hash() == expect
+    assert ModelConfig.from_dict(c.to_dict()) == c
+
+
+def test_token_sets_match_reference():
+    cfg = ModelConfig()
+    oc = om.Config()
+    for a, b in zip(token_sets(cfg), om.token_sets(oc)):
+        assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ process groups (comm.py:319-361)
+def test_process_groups():
+    assert ProcessGroup.dp_groups(8, 2) == [[0, 2, 4, 6], [1, 3, 5, 7]]
+    assert ProcessGroup.dp_groups(8, 4) == [[0, 4], [1, 5], [2, 6], [3, 7]]
+    pg = ProcessGroup(8, 4, 5)
+    assert pg.mp_group == [4, 5, 6, 7] and pg.mp_pos == 1 and pg.dp_group == [1, 5] and pg.dp_replicas == 2
+    pg8 = ProcessGroup(8, 8, 3)
+    assert pg8.mp_group == list(range(8))
+    with pytest.raises(ValueError):
+        ProcessGroup(6, 4, 0)
+
+
+# ------------------------------------------------------------------ parameter layouts
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_layout_local_matches_grid_tiles(n, rng):
+    cfg = om.Config()
+    from paper_2507_05753_b200.sharding import grid_shape
+    R, C = grid_shape(n)
+    sets = {"T": om.token_sets(cfg, R) if R > 1 else None, "K": contiguous_split(cfg.d_tok, C)}
+    glob = rng.standard_normal((cfg.tokens, cfg.d_tok))
+    lay = Layout(n, "matrix", glob.shape, row_sets=sets["T"], col_sets=sets["K"])
+    out = np.zeros_like(glob)
+    for pos in range(n):
+        loc = lay.local(glob, pos)
+        assert np.array_equal(loc, om.local_tile(cfg, "block0.tok1.w", glob, R, C, pos // C, pos % C))
+        lay.place(out, pos, loc)
+    assert np.array_equal(out, glob)
+    # dup positions of a column vector = the column group; of tok2.b = the row group
+    vcol = Layout(n, "vec_col", (cfg.d_emb,), col_sets=contiguous_split(cfg.d_emb, C))
+    vrow = Layout(n, "vec_row", (cfg.tokens,), row_sets=sets["T"])
+    for pos in range(n):
+        r, c = pos // C, pos % C
+        assert vcol.dup_positions(pos) == (tuple(i * C + c for i in range(R)) if R > 1 else ())
+        assert vrow.dup_positions(pos) == tuple(r * C + j for j in range(C))
+    if n in (2, 4):  # the reference's own rule (model.py:168-173)
+        ref_col = lambda p: (p, p ^ 2) if n == 4 else ()  # noqa: E731
+        ref_row = lambda p: (0, 1) if n == 2 else (p, p ^ 1)  # noqa: E731
+        for pos in range(n):
+            assert sorted(vcol.dup_positions(pos)) == sorted(ref_col(pos))
+            assert sorted(vrow.dup_positions(pos)) == sorted(ref_row(pos))
+
+
+def test_layout_to_local_index():
+    cfg = om.Config()
+    sets = om.token_sets(cfg, 2)
+    lay = Layout(4, "matrix", (cfg.tokens, cfg.d_tok), row_sets=sets, col_sets=contiguous_split(cfg.d_tok, 2))
+    t = int(sets[1][5])
+    assert lay.to_local_index(3, (t, 70)) == (5, 6)
+    assert lay.to_local_index(0, (t, 70)) is None
+
+
+# ------------------------------------------------------------------ analytic volume (product copy)
+def test_product_comm_volume_matches_reference_tables():
+    meta = json.load(open(os.path.join(GOLD, "comm_golden.json")))
+    for key, val in meta["primitive_send_elements"].items():
+        mode, n, a_s, b_s = key.split("/")
+        if isinstance(val, str):
+            continue
+        assert primitive_send_elements(mode, int(n), eval(a_s), eval(b_s)) == val, key
+    for key, (fwd, bwd) in meta["comm_volume"].items():
+        mode, n, dims = key.split("/")
+        m, k, no, b = dims.split(",")
+        rep = comm_volume(int(m), int(k), int(no), int(n), mode, batch=int(b[1:]))
+        assert (rep.forward_sent, rep.backward_sent) == (fwd, bwd), key
+        assert rep.total_sent == sum(fwd) + sum(bwd) == rep.total_received

@@ -28,7 +28,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out_q, r):
+def _worker(rank, world, port, out_q, r, mode="fwdbwd"):
     try:
         import sys
         sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -51,6 +51,24 @@ def _worker(rank, world, port, out_q, r):
         g = z["g_out"][:1] if r > 1 else z["g_out"]
         xl = om.local_sample(oc, x, ctx.R, ctx.C, ctx.r, ctx.c)
         gl = om.local_sample(oc, g, ctx.R, ctx.C, ctx.r, ctx.c)
+        if mode == "train":
+            from paper_2507_05753_b200.engine import TrainStep
+            tl = om.local_sample(oc, z["g_out"][:1] * 0.5, ctx.R, ctx.C, ctx.r, ctx.c)  # a target
+            step = TrainStep(model, batch=1, graph=False)
+            losses = []
+            for _ in range(2):
+                step.ws.xin.copy_(torch.tensor(xl[:1], dtype=torch.float32))
+                step.target.copy_(torch.tensor(tl, dtype=torch.float32))
+                step._body()
+                losses.append(float(step.ws.loss.item()))
+            res = {"pos": ctx.pos, "rc": (ctx.R, ctx.C, ctx.r, ctx.c), "losses": losses,
+                   "params": {k: p.data.numpy().copy() for k, p in model.params.items()}}
+            out_q.put(res)
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+                dist.destroy_process_group()
+            return
         model.zero_grads()
         out = model.forward(torch.tensor(xl, dtype=torch.float32), r=r)
         model.backward(torch.tensor(gl, dtype=torch.float32))
@@ -66,11 +84,11 @@ def _worker(rank, world, port, out_q, r):
         out_q.put({"error": traceback.format_exc(), "rank": rank})
 
 
-def _run(world, r=1):
+def _run(world, r=1, mode="fwdbwd"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(rk, world, port, q, r)) for rk in range(world)]
+    procs = [ctx.Process(target=_worker, args=(rk, world, port, q, r, mode)) for rk in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -113,3 +131,34 @@ def test_jigsaw_grid_matches_reference(world):
 
 def test_jigsaw_rollout_4way():
     _check(4, r=2)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_train_step_fused_adam_matches_oracle(world):
+    """Two full TrainStep bodies (fused Adam in the weight-gradient epilogues, vector Adam after
+    the duplicated-gradient sync) reproduce the oracle's SPEC loss + Adam, tile by tile."""
+    from oracle import model as om, train as ot
+    z = np.load(os.path.join(GOLD, "wm_golden.npz"))
+    meta = json.load(open(os.path.join(GOLD, "comm_golden.json")))
+    oc = om.Config(**{**meta["config"], "grid": tuple(meta["config"]["grid"]), "patch": tuple(meta["config"]["patch"])})
+    x, t = z["x"][:1], z["g_out"][:1] * 0.5
+    params = om.init_params(oc, 0, np.float64)
+    mom = {k: np.zeros_like(v) for k, v in params.items()}
+    vel = {k: np.zeros_like(v) for k, v in params.items()}
+    ref_losses = []
+    for step in (1, 2):
+        model = om.SerialModel(oc, params)
+        loss, g = ot.weighted_mse_loss(model.forward(x), t, ot.lat_weights(oc.grid[0]), np.ones(oc.n_vars))
+        grads = model.backward(g)
+        ref_losses.append(loss)
+        for k in params:
+            lr = 2e-5 if k.split(".")[0] in ("enc", "dec") else 1e-4
+            ot.adam_step(params[k], grads[k], mom[k], vel[k], step, lr)
+    res = _run(world, mode="train")
+    p0 = om.init_params(oc, 0, np.float64)
+    for d in res:
+        assert np.allclose(d["losses"], ref_losses, rtol=1e-5), (d["losses"], ref_losses)
+        R, C, rr, cc = d["rc"]
+        upd_got = np.concatenate([(d["params"][k] - om.local_tile(oc, k, p0[k], R, C, rr, cc)).ravel() for k in params])
+        upd_ref = np.concatenate([(om.local_tile(oc, k, params[k] - p0[k], R, C, rr, cc)).ravel() for k in params])
+        assert np.linalg.norm(upd_got - upd_ref) / np.linalg.norm(upd_ref) < 1e-3
