@@ -31,10 +31,10 @@ CONFIGS = {
     # id: (ModelConfig kwargs, real rows, real vars, description)
     "C1": (dict(n_vars=8, grid=(32, 64), patch=(4, 4), d_emb=64, d_tok=128, d_ch=64, n_blocks=4), 32, 8,
            "tiny WeatherMixer (4 blocks, 32x64, 8 vars)"),
-    "C2": (dict(n_vars=70, grid=(32, 64), patch=(2, 2), d_emb=512, d_tok=1024, d_ch=512, n_blocks=12), 32, 69,
-           "WeatherMixer 5.625 deg (32x64, 69->70 ch, 12 blocks)"),
-    "C3": (dict(n_vars=70, grid=(128, 256), patch=(4, 4), d_emb=1024, d_tok=2048, d_ch=1024, n_blocks=12), 128, 69,
-           "WeatherMixer 1.40625 deg (128x256, 69->70 ch, 12 blocks)"),
+    "C2": (dict(n_vars=72, grid=(32, 64), patch=(2, 2), d_emb=512, d_tok=1024, d_ch=512, n_blocks=12), 32, 69,
+           "WeatherMixer 5.625 deg (32x64, 69->72 ch, 12 blocks)"),
+    "C3": (dict(n_vars=72, grid=(128, 256), patch=(4, 4), d_emb=1024, d_tok=2048, d_ch=1024, n_blocks=12), 128, 69,
+           "WeatherMixer 1.40625 deg (128x256, 69->72 ch, 12 blocks)"),
     "C4": (dict(n_vars=70, grid=(728, 1440), patch=(8, 8), d_emb=4320, d_tok=8640, d_ch=4320, n_blocks=3), 721, 69,
            "WeatherMixer 0.25 deg ERA5-shaped (721->728 x 1440, 69->70 ch, 3 blocks, 1.0B params)"),
 }
@@ -290,8 +290,12 @@ def run_ours(args, rank, world):
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        # NCCL communicators captured into a CUDA graph must not be torn down while the graph
+        # lives (destroy_process_group can block); every rank leaves after a final barrier.
         dist.barrier()
-        dist.destroy_process_group()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
 
 
 def main():

@@ -78,6 +78,13 @@ class ModelConfig:
                     raise ConfigError(f"model.{name} must be divisible by {R} for {n}-way sharding")
             if self.patch_features % R:
                 raise ConfigError(f"model patch features ({self.patch_features}) must be divisible by {R}")
+        # TMA row strides are 16-byte multiples: every per-rank contiguous width (bf16) must be a
+        # multiple of 8 elements. Pad n_vars (zero-weight channels) when the patch features miss it.
+        for name, width in (("d_emb", self.d_emb), ("d_tok", self.d_tok), ("d_ch", self.d_ch),
+                            ("n_vars (patch features)", self.patch_features)):
+            if (width // C) % 8:
+                raise ConfigError(f"model.{name}: per-rank width {width // C} at {n}-way must be a multiple of 8 "
+                                  f"(16-byte TMA rows); pad the global width")
 
     def to_dict(self) -> dict:
         return {

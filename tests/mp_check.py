@@ -64,11 +64,11 @@ def main():
     for dtype in ("f32", "bf16"):
         results[f"G1_{dtype}"] = run_case(ctx, meta["config"], dtype, z["x"], z["g_out"], z["out_f64"], gref)
     # C2 scale against the oracle (f64), computed on every rank (cheap)
-    c2 = dict(n_vars=70, grid=(32, 64), patch=(2, 2), d_emb=512, d_tok=1024, d_ch=512, n_blocks=12)
+    c2 = dict(n_vars=72, grid=(32, 64), patch=(2, 2), d_emb=512, d_tok=1024, d_ch=512, n_blocks=12)
     oc = om.Config(**c2)
     rng = np.random.default_rng(1)
-    x = rng.standard_normal((1, 32, 64, 70))
-    g = rng.standard_normal((1, 32, 64, 70))
+    x = rng.standard_normal((1, 32, 64, 72))
+    g = rng.standard_normal((1, 32, 64, 72))
     ref = om.SerialModel(oc, om.init_params(oc, 0, np.float64))
     out_ref = ref.forward(x)
     grads_ref = ref.backward(g)
