@@ -193,6 +193,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t epi = p.epi;
+    float bc1 = 1.f, bc2 = 1.f;
+    const float ab1 = p.adam_b1, ab2 = p.adam_b2, alr = p.adam_lr, aeps = p.adam_eps;
+    if (epi & JG_EPI_ADAM) {
+      const int t = *p.adam_step;
+      bc1 = 1.0f / (1.0f - powf(ab1, (float)t));
+      bc2 = 1.0f / (1.0f - powf(ab2, (float)t));
+    }
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
       const int rem = tile - tb * tiles_per_batch;
@@ -282,32 +289,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           }
         }
         if (epi & JG_EPI_ADAM) {
-          // v[] is the complete gradient of this weight tile: update D (= master) in place
-          const float* mp = p.adam_m;
-          const int t = *p.adam_step;
-          const float bc1 = 1.0f / (1.0f - powf(p.adam_b1, (float)t));
-          const float bc2 = 1.0f / (1.0f - powf(p.adam_b2, (float)t));
+          // v[] is the complete gradient of this weight tile: update D (= master) in place.
+          // All 3 x 8 sixteen-byte loads of the chunk are issued before any math so each thread
+          // keeps ~384 B in flight (the epilogue is HBM-bound: 26 B per parameter).
           float* dp = reinterpret_cast<float*>(p.d);
-          (void)mp;
           if (full_chunk) {
+            float4 w4[8], m4[8], v4[8];
+            const float4* wsrc = reinterpret_cast<const float4*>(dp + drow + col0);
+            const float4* msrc = reinterpret_cast<const float4*>(p.adam_m + drow + col0);
+            const float4* vsrc = reinterpret_cast<const float4*>(p.adam_v + drow + col0);
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              float w[8], mm[8], vv[8];
-              const int64_t o = drow + col0 + g8 * 8;
-              jgd::load8(dp, o, false, w);
-              jgd::load8(p.adam_m, o, false, mm);
-              jgd::load8(p.adam_v, o, false, vv);
+            for (int i = 0; i < 8; ++i) {
+              w4[i] = wsrc[i];
+              m4[i] = msrc[i];
+              v4[i] = vsrc[i];
+            }
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float gj = v[g8 * 8 + j];
-                mm[j] = p.adam_b1 * mm[j] + (1.0f - p.adam_b1) * gj;
-                vv[j] = p.adam_b2 * vv[j] + (1.0f - p.adam_b2) * gj * gj;
-                w[j] -= p.adam_lr * (mm[j] * bc1) / (sqrtf(vv[j] * bc2) + p.adam_eps);
+            for (int i = 0; i < 8; ++i) {
+              float* w = &w4[i].x;
+              float* mm = &m4[i].x;
+              float* vv = &v4[i].x;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float gj = v[i * 4 + j];
+                mm[j] = ab1 * mm[j] + (1.0f - ab1) * gj;
+                vv[j] = ab2 * vv[j] + (1.0f - ab2) * gj * gj;
+                w[j] -= alr * (mm[j] * bc1) / (sqrtf(vv[j] * bc2) + aeps);
               }
-              jgd::store8(dp, o, false, w);
-              jgd::store8(p.adam_m, o, false, mm);
-              jgd::store8(p.adam_v, o, false, vv);
-              if (p.adam_pbf16) jgd::store8(p.adam_pbf16, o, true, w);
+            }
+            float4* wdst = reinterpret_cast<float4*>(dp + drow + col0);
+            float4* mdst = reinterpret_cast<float4*>(p.adam_m + drow + col0);
+            float4* vdst = reinterpret_cast<float4*>(p.adam_v + drow + col0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              wdst[i] = w4[i];
+              mdst[i] = m4[i];
+              vdst[i] = v4[i];
+            }
+            if (p.adam_pbf16) {
+              uint4* bdst = reinterpret_cast<uint4*>(p.adam_pbf16 + drow + col0);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                uint4 raw;
+                __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+                h[0] = __floats2bfloat162_rn(w4[2 * i].x, w4[2 * i].y);
+                h[1] = __floats2bfloat162_rn(w4[2 * i].z, w4[2 * i].w);
+                h[2] = __floats2bfloat162_rn(w4[2 * i + 1].x, w4[2 * i + 1].y);
+                h[3] = __floats2bfloat162_rn(w4[2 * i + 1].z, w4[2 * i + 1].w);
+                bdst[i] = raw;
+              }
             }
           } else {
 #pragma unroll
@@ -315,9 +345,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
               if (j < ncol) {
                 const int64_t o = drow + col0 + j;
                 const float gj = v[j];
-                const float mm = p.adam_b1 * p.adam_m[o] + (1.0f - p.adam_b1) * gj;
-                const float vv = p.adam_b2 * p.adam_v[o] + (1.0f - p.adam_b2) * gj * gj;
-                const float w = dp[o] - p.adam_lr * (mm * bc1) / (sqrtf(vv * bc2) + p.adam_eps);
+                const float mm = ab1 * p.adam_m[o] + (1.0f - ab1) * gj;
+                const float vv = ab2 * p.adam_v[o] + (1.0f - ab2) * gj * gj;
+                const float w = dp[o] - alr * (mm * bc1) / (sqrtf(vv * bc2) + aeps);
                 dp[o] = w;
                 p.adam_m[o] = mm;
                 p.adam_v[o] = vv;

@@ -287,17 +287,24 @@ __global__ void rowsum_kernel(const void* __restrict__ x, bool bf16, float* __re
 
 // ---------------------------------------------------------------- patch permutes
 // token t = gi*gw + gj ; feature f = c*pl*pw + i*pw + j ; grid (gi*pl+i, gj*pw+j, c)
+// One CTA per patch (grid-stride over tokens): the patch's p_lat rows of p_lon*C contiguous
+// grid values are read coalesced into smem laid out [C][p_lat*p_lon + 1] (the +1 pad makes
+// the channel-strided accesses bank-conflict free), then written as one contiguous token row.
 __global__ void patchify_kernel(const float* __restrict__ x, void* __restrict__ tok, bool bf16, int64_t batch,
                                 int64_t lat, int64_t lon, int64_t chans, int64_t pl, int64_t pw) {
+  extern __shared__ float sm[];
   const int64_t gw = lon / pw, T = (lat / pl) * gw, F = chans * pl * pw;
-  const int64_t n = batch * T * F;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = idx % F;
-    const int64_t t = (idx / F) % T;
-    const int64_t b = idx / (F * T);
-    const int64_t c = f / (pl * pw), i = (f / pw) % pl, j = f % pw;
-    const int64_t gi = t / gw, gj = t % gw;
-    jgd::store1(tok, idx, bf16, x[((b * lat + gi * pl + i) * lon + gj * pw + j) * chans + c]);
+  const int PP = static_cast<int>(pl * pw), PS = PP + 1;
+  for (int64_t tk = blockIdx.x; tk < batch * T; tk += gridDim.x) {
+    const int64_t b = tk / T, t = tk % T, gi = t / gw, gj = t % gw;
+    for (int64_t e = threadIdx.x; e < F; e += blockDim.x) {
+      const int64_t c = e % chans, j = (e / chans) % pw, i = e / (chans * pw);
+      sm[c * PS + i * pw + j] = x[((b * lat + gi * pl + i) * lon + gj * pw + j) * chans + c];
+    }
+    __syncthreads();
+    for (int64_t f = threadIdx.x; f < F; f += blockDim.x)
+      jgd::store1(tok, tk * F + f, bf16, sm[(f / PP) * PS + f % PP]);
+    __syncthreads();
   }
 }
 
@@ -317,8 +324,10 @@ __global__ void unpatchify_kernel(const float* __restrict__ tok, float* __restri
 }
 
 // ---------------------------------------------------------------- blend + loss
-// One thread per grid element (coalesced over [B,lat,lon,C]); gathers / scatters the token
-// layout. Per-channel blend gradient and the loss are block-reduced in shared memory.
+// One CTA per patch (grid-stride): the decoder token row is read contiguously into smem
+// [C][p_lat*p_lon + 1]; x / target / out are touched in grid order (coalesced runs of
+// p_lon*C); the gradient token row is staged in smem and written contiguously. Per-channel
+// blend gradients and the loss accumulate in smem; one atomic per channel per CTA.
 constexpr int MAX_CH = 1024;
 __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float* __restrict__ x,
                                   const float* __restrict__ target, const float* __restrict__ blend_w,
@@ -327,50 +336,62 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
                                   float* __restrict__ g_blend, float* __restrict__ g_dec_f32,
                                   __nv_bfloat16* __restrict__ g_dec_bf16, int64_t batch, int64_t lat, int64_t lon,
                                   int64_t chans, int64_t pl, int64_t pw, float inv_count, float loss_scale) {
+  extern __shared__ float sm[];
   __shared__ float s_gb[MAX_CH];
   __shared__ float s_loss[32];
-  for (int c = threadIdx.x; c < chans; c += blockDim.x) s_gb[c] = 0.f;
-  __syncthreads();
   const int64_t gw = lon / pw, T = (lat / pl) * gw, F = chans * pl * pw;
-  const int64_t n = batch * lat * lon * chans;
+  const int PP = static_cast<int>(pl * pw), PS = PP + 1;
+  float* sdec = sm;                 // [C][PS]
+  float* sgd = sm + chans * PS;     // [C][PS]
+  const bool want_grad = (g_ext != nullptr) || (target != nullptr);
+  for (int c = threadIdx.x; c < chans; c += blockDim.x) s_gb[c] = 0.f;
   float lsum = 0.f;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = idx % chans;
-    const int64_t xo = (idx / chans) % lon;
-    const int64_t ya = (idx / (chans * lon)) % lat;
-    const int64_t b = idx / (chans * lon * lat);
-    const int64_t t = (ya / pl) * gw + xo / pw;
-    const int64_t f = c * pl * pw + (ya % pl) * pw + (xo % pw);
-    const int64_t to = (b * T + t) * F + f;
-    const float dec = dec_tok[to];
-    const float xv = x[idx];
-    const float w = blend_w[c];
-    const float o = w * dec + (1.0f - w) * xv;
-    if (out) out[idx] = o;
-    if (!g_ext && !target) continue;  // forward only
-    float g;
-    if (g_ext) {
-      g = g_ext[idx];
-    } else {
-      const float wt = lat_w[ya] * var_w[c];
-      const float e = o - target[idx];
-      lsum += wt * e * e;
-      g = 2.0f * wt * e * inv_count * loss_scale;
+  for (int64_t tk = blockIdx.x; tk < batch * T; tk += gridDim.x) {
+    const int64_t b = tk / T, t = tk % T, gi = t / gw, gj = t % gw;
+    __syncthreads();
+    for (int64_t f = threadIdx.x; f < F; f += blockDim.x) sdec[(f / PP) * PS + f % PP] = dec_tok[tk * F + f];
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < F; e += blockDim.x) {
+      const int64_t c = e % chans, j = (e / chans) % pw, i = e / (chans * pw);
+      const int64_t ya = gi * pl + i;
+      const int64_t ga = ((b * lat + ya) * lon + gj * pw + j) * chans + c;
+      const int si = static_cast<int>(c * PS + i * pw + j);
+      const float dec = sdec[si];
+      const float xv = x[ga];
+      const float w = blend_w[c];
+      const float o = w * dec + (1.0f - w) * xv;
+      if (out) out[ga] = o;
+      if (!want_grad) continue;
+      float g;
+      if (g_ext) {
+        g = g_ext[ga];
+      } else {
+        const float wt = lat_w[ya] * var_w[c];
+        const float er = o - target[ga];
+        lsum += wt * er * er;
+        g = 2.0f * wt * er * inv_count * loss_scale;
+      }
+      atomicAdd(&s_gb[c], g * (dec - xv));
+      sgd[si] = g * w;
     }
-    atomicAdd(&s_gb[c], g * (dec - xv));
-    const float gd = g * w;
-    if (g_dec_f32) g_dec_f32[to] = gd;
-    if (g_dec_bf16) g_dec_bf16[to] = __float2bfloat16_rn(gd);
+    if (!want_grad) continue;
+    __syncthreads();
+    for (int64_t f = threadIdx.x; f < F; f += blockDim.x) {
+      const float gd = sgd[(f / PP) * PS + f % PP];
+      if (g_dec_f32) g_dec_f32[tk * F + f] = gd;
+      if (g_dec_bf16) g_dec_bf16[tk * F + f] = __float2bfloat16_rn(gd);
+    }
   }
+  __syncthreads();
   lsum = warp_sum(lsum);
   if ((threadIdx.x & 31) == 0) s_loss[threadIdx.x >> 5] = lsum;
   __syncthreads();
   if (threadIdx.x < 32) {
     float v = threadIdx.x < (blockDim.x >> 5) ? s_loss[threadIdx.x] : 0.f;
     v = warp_sum(v);
-    if (threadIdx.x == 0 && loss_sum && !g_ext) atomicAdd(loss_sum, v * inv_count);
+    if (threadIdx.x == 0 && loss_sum && target && !g_ext) atomicAdd(loss_sum, v * inv_count);
   }
-  if (g_blend && (g_ext || target))
+  if (g_blend && want_grad)
     for (int c = threadIdx.x; c < chans; c += blockDim.x) atomicAdd(g_blend + c, s_gb[c]);
 }
 
@@ -613,10 +634,15 @@ int jg_patchify(const float* x, void* tokens, int32_t t_type, int64_t batch, int
   JG_SHAPE_CHECK(p_lat > 0 && p_lon > 0 && lat % p_lat == 0 && lon % p_lon == 0,
                  "grid %lldx%lld not divisible by patch %lldx%lld", (long long)lat, (long long)lon, (long long)p_lat,
                  (long long)p_lon);
-  const int64_t n = batch * lat * lon * chans;
-  if (n == 0) return JG_OK;
-  patchify_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, tokens, t_type == JG_BF16, batch, lat, lon,
-                                                                     chans, p_lat, p_lon);
+  const int64_t ntok = batch * (lat / p_lat) * (lon / p_lon);
+  if (ntok == 0) return JG_OK;
+  const int64_t smem = chans * (p_lat * p_lon + 1) * 4;
+  JG_SHAPE_CHECK(smem <= 200 * 1024, "jg_patchify: patch of %lld features too large", (long long)(chans * p_lat * p_lon));
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(patchify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = static_cast<int>(ntok < jg::num_sms() * 8 ? ntok : jg::num_sms() * 8);
+  patchify_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(x, tokens, t_type == JG_BF16, batch, lat, lon, chans,
+                                                             p_lat, p_lon);
   JG_LAUNCH_CHECK("patchify");
   return JG_OK;
 }
@@ -639,9 +665,14 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
   JG_SHAPE_CHECK(chans <= MAX_CH, "jg_blend_loss: at most %d channels", MAX_CH);
   JG_SHAPE_CHECK(lat % p_lat == 0 && lon % p_lon == 0, "jg_blend_loss: grid not divisible by patch");
   JG_SHAPE_CHECK(!target || (lat_w && var_w), "jg_blend_loss: a target needs lat/var weights");
-  const int64_t n = batch * lat * lon * chans;
-  if (n == 0) return JG_OK;
-  blend_loss_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+  const int64_t ntok = batch * (lat / p_lat) * (lon / p_lon);
+  if (ntok == 0) return JG_OK;
+  const int64_t smem = 2 * chans * (p_lat * p_lon + 1) * 4;
+  JG_SHAPE_CHECK(smem <= 180 * 1024, "jg_blend_loss: patch of %lld features too large", (long long)(chans * p_lat * p_lon));
+  if (smem > 40 * 1024)
+    cudaFuncSetAttribute(blend_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = static_cast<int>(ntok < jg::num_sms() * 4 ? ntok : jg::num_sms() * 4);
+  blend_loss_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
       dec_tok, x, target, blend_w, lat_w, var_w, g_out_ext, out, loss_sum, g_blend, g_dec_f32,
       (__nv_bfloat16*)g_dec_bf16, batch, lat, lon, chans, p_lat, p_lon, inv_count, loss_scale);
   JG_LAUNCH_CHECK("blend_loss");
