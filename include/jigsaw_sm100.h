@@ -91,20 +91,36 @@ typedef struct jg_gemm_desc {
    * copy of the updated weight (same indexing), step counter t >= 1 on the device. */
   float* adam_m; float* adam_v; void* adam_pbf16; const int32_t* adam_step;
   float adam_lr, adam_beta1, adam_beta2, adam_eps;
+  /* Per-output-batch destination override (Jigsaw fused reduce-scatter): when d_planes[b] is
+   * non-NULL, batch b of D is written at d_planes[b] (row stride ldd) — typically a peer GPU's
+   * symmetric buffer reached over NVLink — and the epilogue ends with a system-scope fence. */
+  void* d_planes[8];
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);
 
 /*
  * jg_epilogue — the jg_gemm epilogue (same descriptor fields: m, n, batch, epi, alpha, d, d2,
- * bias, resid, pre, stats; A/B fields ignored) applied to an fp32 accumulator acc[b][m][lda]
- * that arrived by another route: the NCCL reduce-scatter of Jigsaw partial products
+ * bias, resid, pre, stats; A/B fields ignored) applied to an accumulator that arrived by
+ * another route: the sum of `nplanes` partial-product planes acc[p][m][lda] (plane stride
+ * acc_bstride, fp32 or bf16) pushed by the Jigsaw peers into this rank's buffer
  * (parallel.py:118-132 sums partials; the bias/GELU/residual follow, parallel.py:521-525).
+ * With nplanes == 1 and desc->batch > 1, acc_bstride is the batch stride instead.
  */
-int jg_epilogue(const jg_gemm_desc* desc, const float* acc, int64_t lda, int64_t acc_bstride, void* stream);
+int jg_epilogue(const jg_gemm_desc* desc, const void* acc, int32_t acc_type, int64_t lda, int64_t acc_bstride,
+                int32_t nplanes, void* stream);
 
 /* y += alpha * x (fp32): accumulate a reduce-scattered weight gradient (parallel.py:490-493). */
 int jg_axpy(float* y, const float* x, float alpha, int64_t n, void* stream);
+
+/* y = sum of nplanes fp32 planes x[p*plane_stride + i] (+ y if accumulate): reduce pushed
+ * Jigsaw partials that need no epilogue (weight gradients). */
+int jg_sum_planes(float* y, const float* x, int64_t n, int32_t nplanes, int64_t plane_stride, int32_t accumulate,
+                  void* stream);
+
+/* Asynchronous device copy (copy engine; either side may be a peer GPU's buffer over NVLink).
+ * Used to push Jigsaw activation tiles into peers' symmetric gather buffers. */
+int jg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
 /* Split fp32 x into tf32-exact hi (low 13 mantissa bits cleared) and lo = x - hi. */
 int jg_split_tf32(const float* x, float* hi, float* lo, int64_t n, void* stream);

@@ -33,7 +33,7 @@ EXPORTED = [
     "jg_gemm", "jg_split_tf32", "jg_split_tf32_2d", "jg_cast_bf16", "jg_gelu_fwd", "jg_gelu_bwd",
     "jg_ln_moments", "jg_ln_apply", "jg_ln_bwd_moments", "jg_ln_bwd_apply",
     "jg_colsum", "jg_rowsum", "jg_patchify", "jg_unpatchify", "jg_blend_loss",
-    "jg_adam", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy",
+    "jg_adam", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async",
     "jg_version", "jg_last_error", "jg_launch_count",
 ]
 
@@ -56,6 +56,7 @@ class GemmDesc(ctypes.Structure):
         ("adam_m", ctypes.c_void_p), ("adam_v", ctypes.c_void_p), ("adam_pbf16", ctypes.c_void_p),
         ("adam_step", ctypes.c_void_p), ("adam_lr", ctypes.c_float), ("adam_beta1", ctypes.c_float),
         ("adam_beta2", ctypes.c_float), ("adam_eps", ctypes.c_float),
+        ("d_planes", ctypes.c_void_p * 8),
     ]
 
 
@@ -93,8 +94,10 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_adam": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp],
         "jg_step_increment": [vp, vp],
         "jg_sqnorm": [vp, i64, vp, vp],
-        "jg_epilogue": [ctypes.POINTER(GemmDesc), vp, i64, i64, vp],
+        "jg_epilogue": [ctypes.POINTER(GemmDesc), vp, i32, i64, i64, i32, vp],
         "jg_axpy": [vp, vp, f32, i64, vp],
+        "jg_sum_planes": [vp, vp, i64, i32, i64, i32, vp],
+        "jg_copy_async": [vp, vp, i64, vp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

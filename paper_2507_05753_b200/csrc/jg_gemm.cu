@@ -50,6 +50,8 @@ struct GemmParams {
   float* stats; int64_t stats_bs;
   float* adam_m; float* adam_v; __nv_bfloat16* adam_pbf16; const int32_t* adam_step;
   float adam_lr, adam_b1, adam_b2, adam_eps;
+  void* d_planes[8];
+  int remote;
 };
 
 template <int BN, bool TF32>
@@ -210,7 +212,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       jgd::mbar_wait(&tfull[acc], acc_phase);
       jgd::tc_fence_after();
 
-      const int64_t drow = tb * p.d_bs + static_cast<int64_t>(row) * p.ldd;
+      // per-batch destination (fused reduce-scatter into a peer's buffer) or the regular strided D
+      void* dbase = p.d;
+      int64_t drow = tb * p.d_bs + static_cast<int64_t>(row) * p.ldd;
+      if (p.remote && tb < 8 && p.d_planes[tb] != nullptr) {
+        dbase = p.d_planes[tb];
+        drow = static_cast<int64_t>(row) * p.ldd;
+      }
       const int64_t d2row = tb * p.d2_bs + static_cast<int64_t>(row) * p.ldd2;
       const int64_t rrow = tb * p.r_bs + static_cast<int64_t>(row) * p.ldr;
       const int64_t prow = tb * p.p_bs + static_cast<int64_t>(row) * p.ldp;
@@ -271,13 +279,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               float t[8];
-              jgd::load8(p.d, drow + col0 + g * 8, false, t);
+              jgd::load8(dbase, drow + col0 + g * 8, false, t);
 #pragma unroll
               for (int j = 0; j < 8; ++j) v[g * 8 + j] += t[j];
             }
           } else {
             #pragma unroll
-            for (int j = 0; j < 32; ++j) if (j < ncol) v[j] += reinterpret_cast<const float*>(p.d)[drow + col0 + j];
+            for (int j = 0; j < 32; ++j) if (j < ncol) v[j] += reinterpret_cast<const float*>(dbase)[drow + col0 + j];
           }
         }
         if (epi & JG_EPI_STATS) {
@@ -390,6 +398,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       jgd::tc_fence_before();
       __syncwarp();
       if (lane == 0) jgd::mbar_arrive(&tempty[acc]);
+      if (p.remote) __threadfence_system();  // peer stores visible before the group barrier
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -504,6 +513,8 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
     return aligned16(ptr) && (ld * es) % 16 == 0;
   };
   JG_SHAPE_CHECK(g->d == nullptr || out_ok(g->d, g->ldd, g->d_type), "jg_gemm: D must be 16B aligned with ld %% 16B == 0");
+  for (int i = 0; i < 8; ++i)
+    JG_SHAPE_CHECK(g->d_planes[i] == nullptr || out_ok(g->d_planes[i], g->ldd, g->d_type), "jg_gemm: misaligned d_planes");
   JG_SHAPE_CHECK(!(epi & JG_EPI_ACCUM) || (g->d && g->d_type == JG_F32), "jg_gemm: ACCUM needs an fp32 D");
   JG_SHAPE_CHECK(!(epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) || (g->d2 && out_ok(g->d2, g->ldd2, g->d2_type)),
                  "jg_gemm: GELU_FWD/COPY_D2 need an aligned D2");
@@ -569,6 +580,13 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   p.adam_m = g->adam_m; p.adam_v = g->adam_v; p.adam_pbf16 = static_cast<__nv_bfloat16*>(g->adam_pbf16);
   p.adam_step = g->adam_step; p.adam_lr = g->adam_lr; p.adam_b1 = g->adam_beta1; p.adam_b2 = g->adam_beta2;
   p.adam_eps = g->adam_eps;
+  p.remote = 0;
+  for (int i = 0; i < 8; ++i) {
+    p.d_planes[i] = g->d_planes[i];
+    if (g->d_planes[i] != nullptr) p.remote = 1;
+  }
+  JG_SHAPE_CHECK(!p.remote || (!g->reduce_batch && g->batch <= 8 && !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM))),
+                 "jg_gemm: d_planes needs <= 8 independent output batches and no ACCUM/ADAM");
 
   if (tf32) {
     if (bn == 256) return launch<256, true>(p, stream);

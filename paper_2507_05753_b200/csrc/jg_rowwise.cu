@@ -464,7 +464,7 @@ struct EpiArgs {
   int64_t m, n;
   uint32_t epi;
   float alpha;
-  const float* acc; int64_t lda, a_bs;
+  const void* acc; int64_t lda, a_bs; int nplanes; bool acc_bf16;
   void* d; int64_t ldd, d_bs; bool d_bf16;
   void* d2; int64_t ldd2, d2_bs; bool d2_bf16;
   const float* bias; int64_t bias_bs;
@@ -481,7 +481,13 @@ __global__ void epilogue_kernel(const EpiArgs a) {
     const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
     float s1 = 0.f, s2 = 0.f;
     for (int64_t c = lane; c < a.n; c += 32) {
-      float v = a.alpha * a.acc[b * a.a_bs + r * a.lda + c];
+      float v = 0.f;
+      if (a.nplanes > 1) {
+        for (int pl = 0; pl < a.nplanes; ++pl) v += jgd::load1(a.acc, pl * a.a_bs + r * a.lda + c, a.acc_bf16);
+      } else {
+        v = jgd::load1(a.acc, b * a.a_bs + r * a.lda + c, a.acc_bf16);
+      }
+      v *= a.alpha;
       if (a.epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
       v += rb;
       if (a.epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
@@ -502,6 +508,15 @@ __global__ void epilogue_kernel(const EpiArgs a) {
         atomicAdd(a.stats + b * a.stats_bs + 2 * r + 1, s2);
       }
     }
+  }
+}
+
+__global__ void sum_planes_kernel(float* __restrict__ y, const float* __restrict__ x, int64_t n, int nplanes,
+                                  int64_t ps, bool accumulate) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = accumulate ? y[i] : 0.f;
+    for (int p = 0; p < nplanes; ++p) s += x[p * ps + i];
+    y[i] = s;
   }
 }
 
@@ -704,8 +719,10 @@ int jg_sqnorm(const float* x, int64_t n, float* out, void* stream) {
   return JG_OK;
 }
 
-int jg_epilogue(const jg_gemm_desc* g, const float* acc, int64_t lda, int64_t acc_bstride, void* stream) {
+int jg_epilogue(const jg_gemm_desc* g, const void* acc, int32_t acc_type, int64_t lda, int64_t acc_bstride,
+                int32_t nplanes, void* stream) {
   JG_SHAPE_CHECK(g && acc && g->m > 0 && g->n > 0 && g->batch > 0, "jg_epilogue: bad shape");
+  JG_SHAPE_CHECK(nplanes >= 1 && (nplanes == 1 || g->batch == 1), "jg_epilogue: planes need batch 1");
   JG_SHAPE_CHECK(!(g->epi & JG_EPI_ACCUM) || (g->d && g->d_type == JG_F32), "jg_epilogue: ACCUM needs an fp32 D");
   JG_SHAPE_CHECK(!(g->epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) || g->d2, "jg_epilogue: missing D2");
   JG_SHAPE_CHECK(!(g->epi & (JG_EPI_BIAS_COL | JG_EPI_BIAS_ROW)) || g->bias, "jg_epilogue: missing bias");
@@ -714,7 +731,7 @@ int jg_epilogue(const jg_gemm_desc* g, const float* acc, int64_t lda, int64_t ac
   JG_SHAPE_CHECK(!(g->epi & JG_EPI_STATS) || g->stats, "jg_epilogue: missing stats");
   EpiArgs a;
   a.m = g->m; a.n = g->n; a.epi = g->epi; a.alpha = g->alpha;
-  a.acc = acc; a.lda = lda; a.a_bs = acc_bstride;
+  a.acc = acc; a.lda = lda; a.a_bs = acc_bstride; a.nplanes = nplanes; a.acc_bf16 = acc_type == JG_BF16;
   a.d = g->d; a.ldd = g->ldd; a.d_bs = g->d_bstride; a.d_bf16 = g->d_type == JG_BF16;
   a.d2 = g->d2; a.ldd2 = g->ldd2; a.d2_bs = g->d2_bstride; a.d2_bf16 = g->d2_type == JG_BF16;
   a.bias = g->bias; a.bias_bs = g->bias_bstride;
@@ -725,6 +742,20 @@ int jg_epilogue(const jg_gemm_desc* g, const float* acc, int64_t lda, int64_t ac
   epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
   JG_LAUNCH_CHECK("epilogue");
   return JG_OK;
+}
+
+int jg_sum_planes(float* y, const float* x, int64_t n, int32_t nplanes, int64_t plane_stride, int32_t accumulate,
+                  void* stream) {
+  if (n == 0) return JG_OK;
+  sum_planes_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(y, x, n, nplanes, plane_stride, accumulate != 0);
+  JG_LAUNCH_CHECK("sum_planes");
+  return JG_OK;
+}
+
+int jg_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes == 0) return JG_OK;
+  return jg::cuda_check(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+                        "cudaMemcpyAsync");
 }
 
 int jg_axpy(float* y, const float* x, float alpha, int64_t n, void* stream) {

@@ -26,53 +26,73 @@ point-to-point schedules (parallel.py:118-353) whose 4-way version is FLOP-imbal
                                     model.py:220-231)
   duplicated-vector gradients       one all-reduce per (lr class, vector kind) (model.py:451-460)
 
-Collectives are NCCL (torch.distributed) on the compute stream, so the whole step stays one
-CUDA graph.
+Exchanges run through transport.py: on B200 the reduce-scatters are fused into the GEMM
+epilogues (partial planes stored straight into the owner's NVLink-mapped buffer) and gathers
+are copy-engine pushes, published by a device barrier — all on the compute stream, so the
+whole step stays one CUDA graph; NCCL (or gloo in the CPU tests) is the alternative transport.
 """
 from __future__ import annotations
+
+import os
 
 import torch
 
 from . import _lib
 from . import kernels as K
+from .transport import NcclTransport, SymmTransport
 
 KM, MN = _lib.JG_KMAJOR, _lib.JG_MNMAJOR
 E_ACC, E_BCOL, E_BROW, E_RES = _lib.EPI_ACCUM, _lib.EPI_BIAS_COL, _lib.EPI_BIAS_ROW, _lib.EPI_RESID
 E_GF, E_GB, E_CP, E_ST = _lib.EPI_GELU_FWD, _lib.EPI_GELU_BWD, _lib.EPI_COPY_D2, _lib.EPI_STATS
 
 CHANNEL_LAYERS = ("enc.w", "ch1.w", "ch2.w", "dec.w")
+F32 = torch.float32
+
+
+def _base(name: str) -> str:
+    return name.split(".", 1)[-1] if name.startswith("block") else name
 
 
 class GridWorkspace:
-    """Gathered panels and collective scratch for one (batch, rollout) shape."""
+    """Transports (row / column group) with their persistent gather slots for one (batch, r)."""
 
     def __init__(self, m, ws):
-        cfg, dev = m.cfg, m.device
+        cfg, dev, ctx = m.cfg, m.device, m.ctx
         R, C = m.R, m.C
         B, nj = ws.B, ws.r * cfg.n_blocks
         E, H, F, Kd = cfg.d_emb, cfg.d_ch, cfg.patch_features, cfg.d_tok
         Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
         M = B * Tl
         od = m.op_dtype
-        f32 = dict(dtype=torch.float32, device=dev)
-        opk = dict(dtype=od, device=dev)
         self.R, self.C = R, C
-        # weight panels: W rows gathered over the column group [N_out, K_in / C]
-        self.panel_shape = {"enc.w": (E, Fl), "ch1.w": (H, El), "ch2.w": (E, Hl), "dec.w": (F, El)}
-        self.panels = {}
-        for name in m.params:
-            base = name.split(".", 1)[-1] if name.startswith("block") else name
-            if base in CHANNEL_LAYERS and R > 1:
-                self.panels[name] = torch.empty(self.panel_shape[base], **opk)
+        self.q = max(1, R // C)  # column-group owner chunks per row-gathered plane
+        panel_shape = {"enc.w": (E, Fl), "ch1.w": (H, El), "ch2.w": (E, Hl), "dec.w": (F, El)}
+        self.panel_names = [n for n in m.params if _base(n) in CHANNEL_LAYERS] if R > 1 else []
+        row_persist = [(f"u_row{j}", (B, C, Tl, El), od) for j in range(nj)]
+        col_persist = []
+        if R > 1:
+            col_persist += [(f"a_col{j}", (B, R, Er, Kl), od) for j in range(nj)]
+            col_persist += [(f"panel:{n}", (R, panel_shape[_base(n)][0] // R, panel_shape[_base(n)][1]), od)
+                            for n in self.panel_names]
+        es, ps = torch.empty((), dtype=od).element_size(), 4
         nmax = max(E, H, F)
+        row_scratch = max(M * nmax * ps, M * nmax * es, Tl * E * ps, Tl * E * es)
         kin_max = max(E * Fl, H * El, E * Hl, F * El)
-        self.scratch = torch.empty(max(M * nmax, kin_max, Tl * E, E * Kl), **f32)
-        self.red = torch.empty(max(M * nmax // C, kin_max // R, Er * Kl, Tl * El), **f32)
-        self.op_scratch = torch.empty(max(M * nmax, Tl * E), **opk)
-        self.op_scratch2 = torch.empty(Tl * E, **opk)
-        self.gh_col = torch.empty(E * Kl, **opk)
-        self.u_row = [torch.empty((B, C, Tl, El), **opk) for _ in range(nj)]
-        self.a_col = [torch.empty((B, E, Kl), **opk) for _ in range(nj)] if R > 1 else None
+        col_scratch = max(E * Kl * ps, kin_max * ps, E * Kl * es)
+        kind = os.environ.get("JIGSAW_TRANSPORT", "symm" if dev.type == "cuda" else "nccl")
+        if kind == "symm":
+            self.row = SymmTransport(ctx.row_group, C, m.c, dev, row_scratch, row_persist) if C > 1 else None
+            self.col = SymmTransport(ctx.col_group, R, m.r, dev, col_scratch, col_persist) if R > 1 else None
+        else:
+            self.row = NcclTransport(ctx.row_group, C, m.c, dev) if C > 1 else None
+            self.col = NcclTransport(ctx.col_group, R, m.r, dev) if R > 1 else None
+            for name, shape, dt in row_persist:
+                self.row.reserve(name, shape, dt)
+            for name, shape, dt in col_persist:
+                self.col.reserve(name, shape, dt)
+        self.kind = kind
+        self.dgrad = torch.empty(max(kin_max, E * Kl), dtype=F32, device=dev)  # reduced weight gradients
+        self.panels = {n: self.col.persistent(f"panel:{n}").view(panel_shape[_base(n)]) for n in self.panel_names}
 
 
 def _gw(m, ws) -> GridWorkspace:
@@ -86,52 +106,139 @@ def _panel(m, g, name):
 
 
 def gather_panels(m, g) -> None:
-    """All-gather every channel-mixing weight over the column group (weights are final for the step)."""
-    for name, buf in g.panels.items():
-        m.ctx.ag_col_into(buf, m.params[name].op)
+    """All-gather every channel-mixing weight's rows over the column group (final for the step)."""
+    for name in g.panel_names:
+        g.col.ag(m.params[name].op, slot=f"panel:{name}")
+
+
+def _wgrad_planes(m, g, wname, acc, nplanes, plane_stride, numel):
+    """Weight gradient that arrived as reduce-scatter planes: sum them into the gradient sink."""
+    if nplanes == 1:
+        m._wgrad_reduced(wname, acc)
+        return
+    red = g.dgrad[:numel]
+    K.sum_planes(red, acc, numel, nplanes, plane_stride)
+    m._wgrad_reduced(wname, red.view(m.params[wname].data.shape))
 
 
 # --------------------------------------------------------------------------- channel layers
 def chan_fwd(m, g, X, panel, M, kin_l, nout, **epi):
-    """Y[M, nout/C] = X[M, kin_l] W^T (+ epilogue), W panel [nout, kin_l]."""
+    """Y[M, nout/C] = X[M, kin_l] W^T (+ epilogue), W panel [nout, kin_l]; RS over the row group."""
     C = m.C
     nl = nout // C
-    P = g.scratch[:C * M * nl].view(C, M, nl)
-    K.gemm(P, X, panel, KM, KM, M, nl, kin_l, C, 0, nl * kin_l, d_bs=M * nl)
-    red = g.red[:M * nl].view(M, nl)
-    m.ctx.rs_row_into(red, P)
-    K.epilogue(red, M, nl, **epi)
+
+    def fn(s, D, d_bs, dpl):
+        K.gemm(D, X, panel, KM, KM, M, nl, kin_l, C, 0, nl * kin_l, d_bs=d_bs, d_planes=dpl)
+
+    acc, npl, ps = g.row.rs_gemm(M, nl, F32, fn)
+    K.epilogue(acc, M, nl, acc_bs=ps, nplanes=npl, **epi)
 
 
 def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None, **dx_epi):
-    """Backward of Y = X W^T: dX (optional, fused epilogue), dW (+= via RS over the column group),
-    bias gradient partial (summed over the column group in grad_sync)."""
+    """Backward of Y = X W^T: dX (optional, fused epilogue), dW via RS over the column group,
+    bias-gradient partial (summed over the column group in grad_sync)."""
     R, C = m.R, m.C
     nl = nout // C
-    dyrow = g.op_scratch[:C * M * nl].view(C, M, nl)
-    m.ctx.ag_row_into(dyrow, dY)
+    dyrow = g.row.ag(dY)                                        # [C, M, nl]
     if dX is not None:
         K.gemm(dX, dyrow, panel, KM, MN, M, kin_l, nl, C, M * nl, nl * kin_l, reduce_batch=True, **dx_epi)
     if R == 1:
         out, kw = m._wgrad(wname)
         K.gemm(out, dyrow, X, MN, MN, nl, kin_l, M, C, M * nl, 0, d_bs=nl * kin_l, **kw)
     else:
-        P = g.scratch[:nout * kin_l].view(C, nl, kin_l)
-        K.gemm(P, dyrow, X, MN, MN, nl, kin_l, M, C, M * nl, 0, d_bs=nl * kin_l)
-        red = g.red[:(nout // R) * kin_l].view(nout // R, kin_l)
-        m.ctx.rs_col_into(red, P.view(R, nout // R, kin_l))
-        m._wgrad_reduced(wname, red)
+        q, nr = g.q, nout // R
+
+        def fn(s, D, d_bs, dpl):  # rows sub-chunk s of every gathered plane j -> owner j*q+s
+            K.gemm(D, dyrow[..., s * nr:], X, MN, MN, nr, kin_l, M, C, M * nl, 0, d_bs=d_bs, d_planes=dpl,
+                   lda=nl)
+
+        acc, npl, ps = g.col.rs_gemm(nr, kin_l, F32, fn, q=q)
+        _wgrad_planes(m, g, wname, acc, npl, ps, nr * kin_l)
     K.colsum(bias_src, m.params[bname].grad, M, nl)
 
 
-# --------------------------------------------------------------------------- forward
+# --------------------------------------------------------------------------- token layers
+def tok1_fwd(m, g, ws, j, bi, b):
+    """h = u^T W1 + b1, a = gelu(h): rows of h (E) gathered over the row group, split R ways."""
+    p, R, C = m.params, m.R, m.C
+    Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
+    urow = g.row.ag(ws.u[j][bi], slot=f"u_row{j}", sub=bi, nsub=ws.B)  # [C, Tl, El]
+    if R == 1:
+        K.gemm(ws.h[j][bi], urow, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
+               epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d2=ws.a[j][bi], d2_bs=El * Kl)
+        return
+    q = g.q
+
+    def fn(s, D, d_bs, dpl):  # rows [s*Er, (s+1)*Er) of plane j -> owner j*q+s
+        K.gemm(D, urow[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C, Tl * El, 0, d_bs=d_bs,
+               d_planes=dpl, lda=El)
+
+    acc, npl, ps = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
+    K.epilogue(acc, Er, Kl, acc_bs=ps, nplanes=npl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data,
+               d=ws.h[j][bi], d2=ws.a[j][bi])
+
+
+def tok2_fwd(m, g, ws, j, bi, b):
+    """x2 = x + W2 a^T + b2[:, None]: a gathered over the column group; RS over the row group."""
+    p, R, C = m.params, m.R, m.C
+    Tl, El, Kl = ws.Tl, ws.El, ws.Kl
+    acol = g.col.ag(ws.a[j][bi], slot=f"a_col{j}", sub=bi, nsub=ws.B).view(-1, Kl) if R > 1 else ws.a[j][bi]
+
+    def fn(s, D, d_bs, dpl):
+        K.gemm(D, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
+
+    acc, npl, ps = g.row.rs_gemm(Tl, El, F32, fn)
+    K.epilogue(acc, Tl, El, acc_bs=ps, nplanes=npl, epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data,
+               resid=ws.res[j][bi], d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
+
+
+def tok2_bwd(m, g, ws, j, bi, b):
+    """gh = (g_x2^T W2) * gelu'(h) (RS over the column group); dW2 += g_x2 a (local)."""
+    p, R, C = m.params, m.R, m.C
+    Tl, El, Er, Kl, B = ws.Tl, ws.El, ws.Er, ws.Kl, ws.B
+    grow = g.row.ag(ws.gx2_op[bi])                              # [C, Tl, El]
+    acol = (g.col.persistent(f"a_col{j}").view(B, -1, Kl)[bi] if R > 1 else ws.a[j][bi])
+    if R == 1:
+        K.gemm(ws.gh[bi], grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
+               epi=E_GB, pre=ws.h[j][bi])
+    else:
+        q = g.q
+
+        def fn(s, D, d_bs, dpl):
+            K.gemm(D, grow[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C, Tl * El, 0, d_bs=d_bs,
+                   d_planes=dpl, lda=El)
+
+        acc, npl, ps = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
+        K.epilogue(acc, Er, Kl, acc_bs=ps, nplanes=npl, epi=E_GB, pre=ws.h[j][bi], d=ws.gh[bi])
+    K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
+    out, kw = m._wgrad(b + "tok2.w") if B == 1 else (p[b + "tok2.w"].grad, {"epi": E_ACC})
+    K.gemm(out, grow, acol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
+
+
+def tok1_bwd(m, g, ws, j, bi, b):
+    """gu = W1 gh^T (gh gathered over the column group, RS over the row group); dW1 += u gh."""
+    p, R, C = m.params, m.R, m.C
+    Tl, El, Kl, B = ws.Tl, ws.El, ws.Kl, ws.B
+    ghcol = g.col.ag(ws.gh[bi]).view(-1, Kl) if R > 1 else ws.gh[bi]
+
+    def fn(s, D, d_bs, dpl):
+        K.gemm(D, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
+
+    acc, npl, ps = g.row.rs_gemm(Tl, El, F32, fn, out=ws.gu[bi])
+    if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
+        K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
+    urow = g.row.persistent(f"u_row{j}").view(B, C, Tl, El)[bi]
+    out, kw = m._wgrad(b + "tok1.w") if B == 1 else (p[b + "tok1.w"].grad, {"epi": E_ACC})
+    K.gemm(out, urow, ghcol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
+
+
+# --------------------------------------------------------------------------- forward / backward
 def forward_grid(m, ws) -> None:
     g = _gw(m, ws)
     cfg, p, ctx = m.cfg, m.params, m.ctx
-    R, C = m.R, m.C
     B = ws.B
     E, H, F = cfg.d_emb, cfg.d_ch, cfg.patch_features
-    Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
+    Tl, El, Hl, Fl = ws.Tl, ws.El, ws.Hl, ws.Fl
     M = B * Tl
     lat, lon = m.local_grid
     ws.stats.zero_()
@@ -146,30 +253,8 @@ def forward_grid(m, ws) -> None:
         K.ln_apply(ws.res[j], ws.st1[j], p[b + "ln1.gamma"].data, p[b + "ln1.beta"].data, ws.u[j], ws.mr1[j],
                    M, El, E, m.eps)
         for bi in range(B):
-            # tok1: h = u^T W1 + b1 ; a = gelu(h)            rows of h: E (gathered), split R ways
-            urow = g.u_row[j][bi]
-            ctx.ag_row_into(urow, ws.u[j][bi])
-            if R == 1:
-                K.gemm(ws.h[j][bi], urow, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
-                       epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d2=ws.a[j][bi], d2_bs=El * Kl)
-            else:
-                P = g.scratch[:E * Kl].view(C, El, Kl)
-                K.gemm(P, urow, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl)
-                red = g.red[:Er * Kl].view(Er, Kl)
-                ctx.rs_col_into(red, P.view(R, Er, Kl))
-                K.epilogue(red, Er, Kl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d=ws.h[j][bi], d2=ws.a[j][bi])
-            # tok2: x2 = x + W2 a^T + b2[:, None]             a gathered over the column group
-            if R > 1:
-                acol = g.a_col[j][bi]
-                ctx.ag_col_into(acol, ws.a[j][bi])
-            else:
-                acol = ws.a[j][bi]
-            P = g.scratch[:C * Tl * El].view(C, Tl, El)
-            K.gemm(P, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=Tl * El)
-            red = g.red[:Tl * El].view(Tl, El)
-            ctx.rs_row_into(red, P)
-            K.epilogue(red, Tl, El, epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data, resid=ws.res[j][bi],
-                       d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
+            tok1_fwd(m, g, ws, j, bi, b)
+            tok2_fwd(m, g, ws, j, bi, b)
         ctx.all_reduce_row(ws.st2[j])
         K.ln_apply(ws.x2[j], ws.st2[j], p[b + "ln2.gamma"].data, p[b + "ln2.beta"].data, ws.v[j], ws.mr2[j],
                    M, El, E, m.eps)
@@ -184,71 +269,34 @@ def forward_grid(m, ws) -> None:
     chan_fwd(m, g, ws.y_op, _panel(m, g, "dec.w"), M, El, F, epi=E_BCOL, bias=p["dec.b"].data, d=ws.dec)
 
 
-# --------------------------------------------------------------------------- backward
 def backward_grid(m, ws) -> None:
     g = _gw(m, ws)
     cfg, p, ctx = m.cfg, m.params, m.ctx
-    R, C = m.R, m.C
     B = ws.B
     E, H, F = cfg.d_emb, cfg.d_ch, cfg.patch_features
     Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
     M = B * Tl
     ws.bstats.zero_()
     gf, gop = ws.g, ws.g_op
-    # decoder: g = gd Wdec (+ bf16 copy)
     cp = gop is not gf
     chan_bwd(m, g, ws.gd, ws.y_op, _panel(m, g, "dec.w"), M, El, F, "dec.w", "dec.b", ws.gd, dX=gf,
              epi=E_CP if cp else 0, d2=gop if cp else None)
     nj = ws.r * cfg.n_blocks
     for j in reversed(range(nj)):
         b = f"block{j % cfg.n_blocks}."
-        # ch2: gc = (g Wc2) * gelu'(c)
         chan_bwd(m, g, gop, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b", gf,
                  dX=ws.gc, epi=E_GB, pre=ws.c[j])
-        # ch1: gv = gc Wc1
         chan_bwd(m, g, ws.gc, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, b + "ch1.w", b + "ch1.b", ws.gc,
                  dX=ws.gv)
         m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, ws.gx2_op, M, El, E,
                   row_reduce=ctx.all_reduce_row)
         for bi in range(B):
-            # tok2 backward: dW2 += sum_e g_x2 a ; gh = (g_x2^T W2) * gelu'(h)
-            grow = g.op_scratch2[:C * Tl * El].view(C, Tl, El)
-            ctx.ag_row_into(grow, ws.gx2_op[bi])
-            acol = g.a_col[j][bi] if R > 1 else ws.a[j][bi]
-            if R == 1:
-                K.gemm(ws.gh[bi], grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
-                       epi=E_GB, pre=ws.h[j][bi])
-            else:
-                P = g.scratch[:E * Kl].view(C, El, Kl)
-                K.gemm(P, grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl)
-                red = g.red[:Er * Kl].view(Er, Kl)
-                ctx.rs_col_into(red, P.view(R, Er, Kl))
-                K.epilogue(red, Er, Kl, epi=E_GB, pre=ws.h[j][bi], d=ws.gh[bi])
-            K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
-            if B == 1:
-                out, kw = m._wgrad(b + "tok2.w")
-            else:  # several samples accumulate: only the plain gradient sink can sum them
-                out, kw = p[b + "tok2.w"].grad, {"epi": E_ACC}
-            K.gemm(out, grow, acol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
+            tok2_bwd(m, g, ws, j, bi, b)
         K.colsum(ws.gh, p[b + "tok1.b"].grad, B * Er, Kl)
         for bi in range(B):
-            # tok1 backward: gu = W1 gh^T (RS over the row group) ; dW1 += sum_e u gh
-            if R > 1:
-                ghcol = g.gh_col[:E * Kl].view(E, Kl)
-                ctx.ag_col_into(ghcol, ws.gh[bi])
-            else:
-                ghcol = ws.gh[bi]
-            P = g.scratch[:C * Tl * El].view(C, Tl, El)
-            K.gemm(P, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=Tl * El)
-            ctx.rs_row_into(ws.gu[bi], P)
-            if B == 1:
-                out, kw = m._wgrad(b + "tok1.w")
-            else:
-                out, kw = p[b + "tok1.w"].grad, {"epi": E_ACC}
-            K.gemm(out, g.u_row[j][bi], ghcol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
+            tok1_bwd(m, g, ws, j, bi, b)
         m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, gop, M, El, E,
                   row_reduce=ctx.all_reduce_row)
-    # encoder: dW only (the input gradient is not needed, model.py:444-445)
     chan_bwd(m, g, gop, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, "enc.w", "enc.b", gf)
 
 

@@ -20,10 +20,11 @@ def gemm(out, a, b, am, bm, m, n, k, *batch_args, **kw):
     return T.gemm_into(out, a, b, am, bm, m, n, k, *batch_args, **kw)
 
 
-def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0,
+def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0,
              d2=None, ldd2=None, d2_bs=0, bias=None, bias_bs=0, resid=None, ldr=None, r_bs=0, pre=None, ldp=None,
              p_bs=0, stats=None, stats_bs=0):
-    """jg_epilogue: the GEMM epilogue applied to an fp32 accumulator `acc` [batch][m][acc_ld]."""
+    """jg_epilogue: the GEMM epilogue applied to an accumulator `acc` [batch][m][acc_ld], or to the
+    sum of `nplanes` partial planes of `acc` (plane stride acc_bs)."""
     g = _lib.GemmDesc()
     g.m, g.n, g.batch, g.epi, g.alpha = m, n, batch, epi, alpha
     g.d, g.ldd, g.d_bstride = ptr(d), ldd if ldd is not None else n, d_bs
@@ -38,7 +39,18 @@ def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, epi=0, alpha=1.0, d=N
         g.pre, g.ldp, g.p_bstride, g.pre_type = pre.data_ptr(), ldp if ldp is not None else n, p_bs, _lib.dtype_code(pre)
     if stats is not None:
         g.stats, g.stats_bstride = stats.data_ptr(), stats_bs
-    _lib.call("jg_epilogue", ctypes.byref(g), acc.data_ptr(), acc_ld if acc_ld is not None else n, acc_bs)
+    _lib.call("jg_epilogue", ctypes.byref(g), acc.data_ptr(), _lib.dtype_code(acc), acc_ld if acc_ld is not None else n,
+              acc_bs, nplanes)
+
+
+def sum_planes(y, x, n, nplanes, plane_stride, accumulate=False):
+    """y[:n] (+)= sum_p x[p * plane_stride + i] (fp32)."""
+    _lib.call("jg_sum_planes", y.data_ptr(), x.data_ptr(), n, nplanes, plane_stride, int(accumulate))
+
+
+def copy_async(dst_ptr: int, src: torch.Tensor, nbytes: int | None = None):
+    """Copy-engine copy of `src` to a raw device address (e.g. a peer's symmetric buffer)."""
+    _lib.call("jg_copy_async", dst_ptr, src.data_ptr(), nbytes if nbytes is not None else src.numel() * src.element_size())
 
 
 def axpy(y, x, alpha=1.0):

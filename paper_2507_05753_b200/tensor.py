@@ -81,7 +81,8 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
               r_bs: int = 0, pre: torch.Tensor | None = None, p_bs: int = 0, stats: torch.Tensor | None = None,
               stats_bs: int = 0, d_bs: int | None = None, d2_bs: int | None = None,
               lda: int | None = None, ldb: int | None = None, ldd: int | None = None,
-              a_lo: torch.Tensor | None = None, b_lo: torch.Tensor | None = None, adam=None) -> torch.Tensor:
+              a_lo: torch.Tensor | None = None, b_lo: torch.Tensor | None = None, adam=None,
+              d_planes=None) -> torch.Tensor:
     """Low-level fused GEMM: out[b] (op)= sum_k A[b](m,k) B[b](n,k) with epilogue `epi`.
 
     A/B majors follow include/jigsaw_sm100.h. fp32 operands run 3xTF32: the hi/lo split is
@@ -118,6 +119,9 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
         d.pre, d.ldp, d.p_bstride, d.pre_type = pre.data_ptr(), n, p_bs if p_bs else m * n, _lib.dtype_code(pre)
     if stats is not None:
         d.stats, d.stats_bstride = stats.data_ptr(), stats_bs if stats_bs else 2 * m
+    if d_planes is not None:
+        for i, addr in enumerate(d_planes):
+            d.d_planes[i] = addr
     if adam is not None:
         # adam = (m_view, v_view, bf16_copy_view | None, step_counter, lr, beta1, beta2, eps); out = master
         am, av, apb, astep, lr, b1, b2, eps = adam

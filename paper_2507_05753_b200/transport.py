@@ -1,0 +1,147 @@
+"""Jigsaw exchange transports for one grid axis (the row group or the column group of a rank).
+
+Two implementations of the same two operations used by jigsaw_grid.py:
+
+  ag(x, slot)          all-gather: returns the local [G, *x.shape] planes of the group members'
+                       blocks (ordered by group index)
+  rs_gemm(shape, fn)   reduce-scatter of a GEMM's partial products: `fn(planes, d_planes)` runs
+                       the plane-batched GEMM; returns (acc, nplanes, plane_stride) for the
+                       consuming epilogue (which sums the planes)
+
+* NcclTransport — NCCL all_gather_into_tensor / reduce_scatter_tensor on the compute stream
+  (also the gloo path of the CPU tests).
+* SymmTransport — NVLink peer memory (torch symmetric memory, CUDA backend): the GEMM epilogue
+  stores each partial plane straight into its owner's buffer (`d_planes`, remote st.global
+  over NVLink, overlapping the transfer with the MMA tile by tile); gathers are copy-engine
+  pushes into the peers' buffers; a 7 us device barrier (graph-capturable) publishes them.
+  Buffers: one symmetric arena per group = persistent slots (gathered tensors that live for the
+  whole step: u rows, gelu(h) columns, weight panels) + two rotating scratch regions, so an
+  exchange never overwrites a region a peer may still be reading (the barrier of exchange k+1
+  orders it after every rank's consumer of exchange k-1).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import kernels as K
+
+
+class NcclTransport:
+    kind = "nccl"
+
+    def __init__(self, group, G: int, idx: int, device):
+        self.group, self.G, self.idx, self.device = group, G, idx, device
+        self._persist: dict[str, torch.Tensor] = {}
+        self._scratch = {}
+
+    def reserve(self, name: str, shape, dtype) -> None:
+        self._persist[name] = torch.empty(shape, dtype=dtype, device=self.device)
+
+    def persistent(self, name: str) -> torch.Tensor:
+        return self._persist[name]
+
+    def _buf(self, key, numel, dtype):
+        b = self._scratch.get((key, dtype))
+        if b is None or b.numel() < numel:
+            b = torch.empty(numel, dtype=dtype, device=self.device)
+            self._scratch[(key, dtype)] = b
+        return b[:numel]
+
+    def ag(self, x: torch.Tensor, slot: str | None = None, sub: int = 0, nsub: int = 1) -> torch.Tensor:
+        """Planes [G, *x.shape]; `slot` = persistent destination (viewed [nsub, G, *x.shape], entry sub)."""
+        if slot is not None:
+            out = self._persist[slot].view(nsub, self.G, *x.shape)[sub]
+        else:
+            out = self._buf("ag", self.G * x.numel(), x.dtype).view(self.G, *x.shape)
+        if self.G == 1:
+            out[0].copy_(x)
+        else:
+            dist.all_gather_into_tensor(out.view(-1), x.reshape(-1), group=self.group)
+        return out
+
+    def rs_gemm(self, rows: int, cols: int, dtype, fn, q: int = 1, out: torch.Tensor | None = None):
+        """fn(s, D, d_bs, d_planes) for s < q computes GEMM batches j writing owner plane j*q + s."""
+        planes = self._buf("rs", self.G * rows * cols, dtype).view(self.G, rows, cols)
+        for s in range(q):
+            fn(s, planes[s], q * rows * cols, None)
+        if self.G == 1:
+            return planes[0], 1, 0
+        red = out if out is not None else self._buf("red", rows * cols, dtype).view(rows, cols)
+        dist.reduce_scatter_tensor(red.view(-1), planes.view(-1), group=self.group)
+        return red, 1, 0
+
+
+class SymmTransport:
+    kind = "symm"
+
+    def __init__(self, group, G: int, idx: int, device, scratch_bytes: int, persist_spec):
+        import torch.distributed._symmetric_memory as symm
+        self.group, self.G, self.idx, self.device = group, G, idx, device
+        self.offsets: dict[str, tuple[int, tuple, torch.dtype]] = {}
+        off = 0
+        for name, shape, dtype in persist_spec:
+            n = 1
+            for s in shape:
+                n *= s
+            self.offsets[name] = (off, tuple(shape), dtype)
+            off += -(-n * torch.empty((), dtype=dtype).element_size() // 256) * 256
+        self.scratch_off = off
+        self.scratch_bytes = -(-scratch_bytes // 256) * 256
+        total = off + 2 * self.scratch_bytes
+        name = group.group_name
+        try:
+            symm.enable_symm_mem_for_group(name)
+        except Exception:  # noqa: BLE001  (newer torch enables on demand)
+            pass
+        self.buf = symm.empty(total, dtype=torch.uint8, device=device)
+        self.hdl = symm.rendezvous(self.buf, name)
+        self.base = [int(p) for p in self.hdl.buffer_ptrs]
+        self.k = 0
+
+    def reserve(self, name, shape, dtype):  # persistent slots are fixed at construction
+        assert name in self.offsets, name
+
+    def _view(self, off: int, shape, dtype) -> torch.Tensor:
+        n = 1
+        for s in shape:
+            n *= s
+        es = torch.empty((), dtype=dtype).element_size()
+        return self.buf[off:off + n * es].view(dtype).view(*shape)
+
+    def persistent(self, name: str) -> torch.Tensor:
+        off, shape, dtype = self.offsets[name]
+        return self._view(off, shape, dtype)
+
+    def _region(self) -> int:
+        r = self.scratch_off + (self.k % 2) * self.scratch_bytes
+        self.k += 1
+        return r
+
+    def barrier(self) -> None:
+        self.hdl.barrier(channel=0)
+
+    def ag(self, x: torch.Tensor, slot: str | None = None, sub: int = 0, nsub: int = 1) -> torch.Tensor:
+        nbytes = x.numel() * x.element_size()
+        if slot is not None:
+            off = self.offsets[slot][0] + sub * self.G * nbytes
+        else:
+            off = self._region()
+            assert self.G * nbytes <= self.scratch_bytes
+        x = x.contiguous()
+        for j in range(self.G):  # push my block into slot idx of every member (copy engine)
+            K.copy_async(self.base[j] + off + self.idx * nbytes, x, nbytes)
+        self.barrier()
+        return self._view(off, (self.G, *x.shape), x.dtype)
+
+    def rs_gemm(self, rows: int, cols: int, dtype, fn, q: int = 1, out: torch.Tensor | None = None):
+        es = torch.empty((), dtype=dtype).element_size()
+        pbytes = rows * cols * es
+        off = self._region()
+        assert self.G * pbytes <= self.scratch_bytes
+        local = self._view(off, (self.G, rows, cols), dtype)
+        # owner plane o of my partial goes to slot idx of member o's region (remote epilogue stores)
+        for s in range(q):
+            fn(s, local[0], 0, [self.base[j * q + s] + off + self.idx * pbytes for j in range(self.G // q)])
+        self.barrier()
+        return local, self.G, rows * cols

@@ -55,7 +55,8 @@ def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias
 
 def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=False, epi=0, alpha=1.0, d2=None,
          bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
-         d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None):
+         d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None, d_planes=None):
+    assert d_planes is None, "the CPU double has no peer memory"
     lda = lda if lda is not None else (k if am == KM else m)
     ldb = ldb if ldb is not None else (k if bm == KM else n)
     ldd = ldd if ldd is not None else n
@@ -66,7 +67,11 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
     stats_bs = stats_bs if stats_bs else 2 * m
     acc = []
     for bi in range(batch):
-        A = _view(a, (m, k), (lda, 1) if am == KM else (1, lda), bi * a_bs).double()
+        try:
+            A = _view(a, (m, k), (lda, 1) if am == KM else (1, lda), bi * a_bs).double()
+        except RuntimeError as e:
+            raise RuntimeError(f"A view: shape {tuple(a.shape)} stride {a.stride()} off {a.storage_offset()} "
+                               f"m={m} n={n} k={k} batch={batch} a_bs={a_bs} lda={lda} am={am}: {e}") from None
         B = _view(b, (n, k), (ldb, 1) if bm == KM else (1, ldb), bi * b_bs).double()
         acc.append(A @ B.T)
     if reduce_batch:
@@ -91,15 +96,25 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
     return out
 
 
-def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0, d2=None,
-             ldd2=None, d2_bs=0, bias=None, bias_bs=0, resid=None, ldr=None, r_bs=0, pre=None, ldp=None, p_bs=0,
-             stats=None, stats_bs=0):
+def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0,
+             d2=None, ldd2=None, d2_bs=0, bias=None, bias_bs=0, resid=None, ldr=None, r_bs=0, pre=None, ldp=None,
+             p_bs=0, stats=None, stats_bs=0):
     acc_ld = acc_ld if acc_ld is not None else n
     for ob in range(batch):
-        v = _view(acc, (m, n), (acc_ld, 1), ob * acc_bs).double()
+        if nplanes > 1:
+            v = sum(_view(acc, (m, n), (acc_ld, 1), p * acc_bs).double() for p in range(nplanes))
+        else:
+            v = _view(acc, (m, n), (acc_ld, 1), ob * acc_bs).double()
         _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd if ldd is not None else n, d_bs, d2,
                         ldd2 if ldd2 is not None else n, d2_bs, bias, bias_bs, resid, ldr if ldr is not None else n,
                         r_bs, pre, ldp if ldp is not None else n, p_bs, stats, stats_bs)
+
+
+def sum_planes(y, x, n, nplanes, plane_stride, accumulate=False):
+    s = sum(x.reshape(-1)[p * plane_stride:p * plane_stride + n].double() for p in range(nplanes))
+    if accumulate:
+        s = s + y.reshape(-1)[:n].double()
+    y.reshape(-1)[:n].copy_(s.float())
 
 
 def axpy(y, x, alpha=1.0):
@@ -214,7 +229,7 @@ def step_increment(counter):
     counter += 1
 
 
-NAMES = ["gemm", "epilogue", "axpy", "cast_bf16", "patchify", "ln_moments", "ln_apply", "ln_bwd_moments",
+NAMES = ["gemm", "epilogue", "sum_planes", "axpy", "cast_bf16", "patchify", "ln_moments", "ln_apply", "ln_bwd_moments",
          "ln_bwd_apply", "colsum", "rowsum", "blend_loss", "adam", "step_increment"]
 
 
