@@ -366,13 +366,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           continue;
         }
         // primary output
-        if (p.d != nullptr) {
+        if (dbase != nullptr) {
           if (full_chunk) {
 #pragma unroll
-            for (int g = 0; g < 4; ++g) jgd::store8(p.d, drow + col0 + g * 8, p.d_bf16, v + g * 8);
+            for (int g = 0; g < 4; ++g) jgd::store8(dbase, drow + col0 + g * 8, p.d_bf16, v + g * 8);
           } else {
-            #pragma unroll
-            for (int j = 0; j < 32; ++j) if (j < ncol) jgd::store1(p.d, drow + col0 + j, p.d_bf16, v[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) if (j < ncol) jgd::store1(dbase, drow + col0 + j, p.d_bf16, v[j]);
           }
         }
         // secondary output: gelu(result) or a plain copy

@@ -27,3 +27,14 @@ def test_jigsaw_nccl_parity(n):
     print(res)
     for key, tol in (("G1_f32", 1e-4), ("C2_f32", 1e-4), ("G1_bf16", 2e-2), ("C2_bf16", 2e-2)):
         assert res[key]["out"] < tol and res[key]["grad"] < tol, (key, res[key])
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_symmetric_memory_transport_matches_nccl(n):
+    """Peer-memory gathers and GEMM-epilogue reduce-scatters equal NCCL's, bit for bit."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29563", os.path.join(HERE, "transport_check.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert "TRANSPORT_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]

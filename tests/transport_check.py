@@ -1,0 +1,47 @@
+"""Compare SymmTransport with NcclTransport on random data (run under torchrun, n = 2 or 4)."""
+import os, sys
+import torch, torch.distributed as dist
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from paper_2507_05753_b200 import Communicator, MpContext, _lib
+from paper_2507_05753_b200 import kernels as K
+from paper_2507_05753_b200.transport import NcclTransport, SymmTransport
+
+comm = Communicator.from_env()
+ctx = MpContext(comm, list(range(comm.world_size)))
+dev = torch.device("cuda", torch.cuda.current_device())
+rank = comm.rank
+torch.manual_seed(rank)
+res = []
+for axis in ("row", "col"):
+    G = ctx.C if axis == "row" else ctx.R
+    if G == 1:
+        continue
+    grp = ctx.row_group if axis == "row" else ctx.col_group
+    idx = ctx.c if axis == "row" else ctx.r
+    st = SymmTransport(grp, G, idx, dev, 64 << 20, [("keep", (3, G, 128, 64), torch.bfloat16)])
+    nt = NcclTransport(grp, G, idx, dev)
+    x = torch.randn(128, 64, device=dev).bfloat16()
+    a = st.ag(x)
+    b = nt.ag(x)
+    res.append((axis, "ag", (a.float() - b.float()).abs().max().item()))
+    a2 = st.ag(x * 2, slot="keep", sub=1, nsub=3)
+    res.append((axis, "ag_slot", (a2.float() - 2 * b.float()).abs().max().item()))
+    # rs_gemm: partial P[G*64, 48] = A[G*64, 96] B[48, 96]^T, planes over output rows
+    A = torch.randn(G * 64, 96, device=dev).bfloat16()
+    Bm = torch.randn(48, 96, device=dev).bfloat16()
+
+    def fn(s, D, d_bs, dpl):
+        K.gemm(D, A, Bm, 0, 0, 64, 48, 96, G, 64 * 96, 0, d_bs=d_bs, d_planes=dpl)
+
+    sa, sn, sp = st.rs_gemm(64, 48, torch.float32, fn)
+    ssum = sum(sa.reshape(-1)[i * sp:(i + 1) * sp] for i in range(sn)).view(64, 48) if sn > 1 else sa
+    na, nn, np_ = nt.rs_gemm(64, 48, torch.float32, fn)
+    res.append((axis, "rs", (ssum - na).abs().max().item(), na.abs().max().item()))
+    torch.cuda.synchronize()
+print(rank, res, flush=True)
+bad = [r for r in res if r[2] != 0.0]
+if rank == 0:
+    print("TRANSPORT_OK" if not bad else f"TRANSPORT_BAD {bad}", flush=True)
+dist.barrier()
+os._exit(0)
