@@ -30,6 +30,9 @@ constexpr int SMEM_BUDGET = 196 * 1024;
 struct GemmParams {
   CUtensorMap tma_a[3];
   CUtensorMap tma_b[3];
+  CUtensorMap tma_d[8];   // D store maps: [0] = batched D, or one per remote output plane
+  CUtensorMap tma_d2;
+  int tma_store;          // 1: epilogue writes D / D2 through TMA bulk tensor stores
   int nseg;
   int m, n, k;
   int batch;
@@ -65,7 +68,8 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;          // double-buffered fp32 accumulator
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_STAGE_BYTES = 4 * 4096;  // one 32x32 fp32 staging tile per epilogue warp
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t IDESC_BASE =
       (1u << 4)                                    // D format: f32
       | ((TF32 ? 2u : 1u) << 7)                    // A format: tf32 / bf16
@@ -74,6 +78,35 @@ struct Cfg {
       | (static_cast<uint32_t>(BM >> 4) << 24);    // M
 };
 
+// Stage one warp's 32 x 32 accumulator chunk (thread = row) in 128B / 64B-swizzled smem and
+// TMA-store it: rows become contiguous bulk writes (HBM or an NVLink peer), conflict-free smem.
+__device__ __forceinline__ void stage_store(uint8_t* stg, const float* v, bool bf16, int lane,
+                                            const CUtensorMap* map, int c0, int c1, int c2) {
+  if (lane == 0) jgd::bulk_wait_read0();
+  __syncwarp();
+  if (bf16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 raw;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * i + 2 * k], v[8 * i + 2 * k + 1]);
+      *reinterpret_cast<uint4*>(stg + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4)) = raw;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      *reinterpret_cast<float4*>(stg + lane * 128 + ((i ^ (lane & 7)) << 4)) =
+          make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  }
+  jgd::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    jgd::tma_store_3d(map, stg, c0, c1, c2);
+    jgd::bulk_commit();
+  }
+}
+
 template <int BN, bool TF32>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
   using C = Cfg<BN, TF32>;
@@ -81,7 +114,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* smem_epi = smem + C::STAGES * C::STAGE_BYTES;  // 1024-aligned: 4 x 4 KB staging tiles
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + C::EPI_STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -192,6 +226,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* stg = smem_epi + (warp - 4) * 4096;
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t epi = p.epi;
@@ -232,9 +267,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
         if (col0 >= p.n) break;  // warp-uniform
         float v[32];
         jgd::tmem_ld32(tmem_base + static_cast<uint32_t>(acc * BN + c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
-        if (!row_ok) continue;
         const bool full_chunk = col0 + 32 <= p.n;
         const int ncol = full_chunk ? 32 : p.n - col0;
+        if (row_ok) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
         if (epi & JG_EPI_BIAS_COL) {
@@ -296,7 +331,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             s2 += x * x;
           }
         }
-        if (epi & JG_EPI_ADAM) {
+        }  // row_ok: math done
+        if ((epi & JG_EPI_ADAM) && row_ok) {
           // v[] is the complete gradient of this weight tile: update D (= master) in place.
           // All 3 x 8 sixteen-byte loads of the chunk are issued before any math so each thread
           // keeps ~384 B in flight (the epilogue is HBM-bound: 26 B per parameter).
@@ -365,6 +401,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           }
           continue;
         }
+        if (p.tma_store) {
+          // stage the warp's 32 x 32 chunk in swizzled smem, one TMA bulk tensor store per output
+          const int rbase = m0 + q * 32;
+          if (p.remote || p.d != nullptr)
+            stage_store(stg, v, p.d_bf16, lane, &p.tma_d[p.remote ? tb : 0], col0, rbase, p.remote ? 0 : tb);
+          if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
+            if (epi & JG_EPI_GELU_FWD) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = jgd::gelu_f(v[j]);
+            }
+            stage_store(stg, v, p.d2_bf16, lane, &p.tma_d2, col0, rbase, tb);
+          }
+          continue;
+        }
+        if (!row_ok) continue;
         // primary output
         if (dbase != nullptr) {
           if (full_chunk) {
@@ -385,7 +436,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
 #pragma unroll
             for (int g = 0; g < 4; ++g) jgd::store8(p.d2, d2row + col0 + g * 8, p.d2_bf16, v + g * 8);
           } else {
-            #pragma unroll
+#pragma unroll
             for (int j = 0; j < 32; ++j) if (j < ncol) jgd::store1(p.d2, d2row + col0 + j, p.d2_bf16, v[j]);
           }
         }
@@ -398,9 +449,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       jgd::tc_fence_before();
       __syncwarp();
       if (lane == 0) jgd::mbar_arrive(&tempty[acc]);
-      if (p.remote) __threadfence_system();  // peer stores visible before the group barrier
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) jgd::bulk_wait0();  // every TMA store of this warp has landed
+    __syncwarp();
+    if (p.remote) __threadfence_system();  // peer stores visible before the group barrier
   }
 
   __syncthreads();
@@ -459,6 +512,35 @@ int make_operand_map(CUtensorMap* map, const void* ptr, bool tf32, bool mn_major
     char buf[256];
     snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d): rows=%lld k=%lld ld=%lld", (int)r,
              (long long)rows, (long long)k, (long long)ld);
+    return jg::shape_error(buf);
+  }
+  return JG_OK;
+}
+
+// Store map for an epilogue output: dims (cols, rows, batches), 32 x 32 boxes, swizzled to match
+// stage_store (128B rows for fp32, 64B rows for bf16).
+int make_store_map(CUtensorMap* map, void* ptr, bool bf16, int64_t rows, int64_t cols, int64_t ld, int64_t bstride,
+                   int64_t batches) {
+  const int es = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batches)};
+  cuuint64_t strides[2];
+  strides[0] = static_cast<cuuint64_t>(ld) * es;
+  strides[1] = batches > 1 ? static_cast<cuuint64_t>(bstride) * es : strides[0] * dims[1];
+  if (strides[1] == 0 || strides[1] % 16) strides[1] = ((strides[0] * dims[1] + 15) / 16) * 16;
+  cuuint32_t box[3] = {32, 32, 1}, estr[3] = {1, 1, 1};
+  auto fn = encode_fn();
+  if (!fn) {
+    jg::set_error("cuTensorMapEncodeTiled unavailable");
+    return JG_ERR_CUDA;
+  }
+  CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[200];
+    snprintf(buf, sizeof(buf), "store tensor map failed (%d): rows=%lld cols=%lld ld=%lld", (int)r, (long long)rows,
+             (long long)cols, (long long)ld);
     return jg::shape_error(buf);
   }
   return JG_OK;
@@ -587,6 +669,24 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   }
   JG_SHAPE_CHECK(!p.remote || (!g->reduce_batch && g->batch <= 8 && !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM))),
                  "jg_gemm: d_planes needs <= 8 independent output batches and no ACCUM/ADAM");
+  // TMA-store epilogue whenever D is write-only (no read-modify-write of D)
+  p.tma_store = !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM)) && (g->d != nullptr || p.remote);
+  if (p.tma_store) {
+    const bool dbf = g->d_type == JG_BF16;
+    if (p.remote) {
+      for (int b = 0; b < static_cast<int>(out_batches); ++b) {
+        int rc = make_store_map(&p.tma_d[b], g->d_planes[b] ? g->d_planes[b] : g->d, dbf, g->m, g->n, g->ldd, 0, 1);
+        if (rc) return rc;
+      }
+    } else {
+      int rc = make_store_map(&p.tma_d[0], g->d, dbf, g->m, g->n, g->ldd, g->d_bstride, out_batches);
+      if (rc) return rc;
+    }
+    if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
+      int rc = make_store_map(&p.tma_d2, g->d2, g->d2_type == JG_BF16, g->m, g->n, g->ldd2, g->d2_bstride, out_batches);
+      if (rc) return rc;
+    }
+  }
 
   if (tf32) {
     if (bn == 256) return launch<256, true>(p, stream);
