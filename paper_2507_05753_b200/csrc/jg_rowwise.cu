@@ -293,17 +293,21 @@ __global__ void rowsum_kernel(const void* __restrict__ x, bool bf16, float* __re
 __global__ void patchify_kernel(const float* __restrict__ x, void* __restrict__ tok, bool bf16, int64_t batch,
                                 int64_t lat, int64_t lon, int64_t chans, int64_t pl, int64_t pw) {
   extern __shared__ float sm[];
-  const int64_t gw = lon / pw, T = (lat / pl) * gw, F = chans * pl * pw;
-  const int PP = static_cast<int>(pl * pw), PS = PP + 1;
+  const int64_t gw = lon / pw, T = (lat / pl) * gw;
+  const int C = static_cast<int>(chans), PL = static_cast<int>(pl), PW = static_cast<int>(pw);
+  const int PP = PL * PW, PS = PP + 1, F = C * PP, RW = PW * C;  // RW: contiguous run per patch row
   for (int64_t tk = blockIdx.x; tk < batch * T; tk += gridDim.x) {
     const int64_t b = tk / T, t = tk % T, gi = t / gw, gj = t % gw;
-    for (int64_t e = threadIdx.x; e < F; e += blockDim.x) {
-      const int64_t c = e % chans, j = (e / chans) % pw, i = e / (chans * pw);
-      sm[c * PS + i * pw + j] = x[((b * lat + gi * pl + i) * lon + gj * pw + j) * chans + c];
+    const float* src = x + ((b * lat + gi * pl) * lon + gj * pw) * chans;
+    for (int e = threadIdx.x; e < F; e += blockDim.x) {
+      const int i = e / RW, r = e - i * RW, j = r / C, c = r - j * C;
+      sm[c * PS + i * PW + j] = src[static_cast<int64_t>(i) * lon * chans + r];
     }
     __syncthreads();
-    for (int64_t f = threadIdx.x; f < F; f += blockDim.x)
-      jgd::store1(tok, tk * F + f, bf16, sm[(f / PP) * PS + f % PP]);
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+      const int c = f / PP, rr = f - c * PP;
+      jgd::store1(tok, tk * F + f, bf16, sm[c * PS + rr]);
+    }
     __syncthreads();
   }
 }
@@ -329,6 +333,8 @@ __global__ void unpatchify_kernel(const float* __restrict__ tok, float* __restri
 // p_lon*C); the gradient token row is staged in smem and written contiguously. Per-channel
 // blend gradients and the loss accumulate in smem; one atomic per channel per CTA.
 constexpr int MAX_CH = 1024;
+// Threads t < C * floor(blockDim / C) each own channel t % C for the whole kernel: the grid
+// element loop strides by a multiple of C, so blend-gradient and loss partials stay in registers.
 __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float* __restrict__ x,
                                   const float* __restrict__ target, const float* __restrict__ blend_w,
                                   const float* __restrict__ lat_w, const float* __restrict__ var_w,
@@ -339,50 +345,62 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
   extern __shared__ float sm[];
   __shared__ float s_gb[MAX_CH];
   __shared__ float s_loss[32];
-  const int64_t gw = lon / pw, T = (lat / pl) * gw, F = chans * pl * pw;
-  const int PP = static_cast<int>(pl * pw), PS = PP + 1;
-  float* sdec = sm;                 // [C][PS]
-  float* sgd = sm + chans * PS;     // [C][PS]
+  const int64_t gw = lon / pw, T = (lat / pl) * gw;
+  const int C = static_cast<int>(chans), PL = static_cast<int>(pl), PW = static_cast<int>(pw);
+  const int PP = PL * PW, PS = PP + 1, F = C * PP, RW = PW * C;
+  float* sdec = sm;          // [C][PS]
+  float* sgd = sm + C * PS;  // [C][PS]
   const bool want_grad = (g_ext != nullptr) || (target != nullptr);
-  for (int c = threadIdx.x; c < chans; c += blockDim.x) s_gb[c] = 0.f;
-  float lsum = 0.f;
+  const int stride = (static_cast<int>(blockDim.x) / C) * C;  // > 0: host guarantees C <= blockDim
+  const int t0 = static_cast<int>(threadIdx.x);
+  const bool active = t0 < stride;
+  const int my_c = active ? t0 % C : 0;
+  const float w = blend_w[my_c], vw = var_w ? var_w[my_c] : 0.f;
+  for (int c = t0; c < C; c += blockDim.x) s_gb[c] = 0.f;
+  float lsum = 0.f, gb = 0.f;
   for (int64_t tk = blockIdx.x; tk < batch * T; tk += gridDim.x) {
     const int64_t b = tk / T, t = tk % T, gi = t / gw, gj = t % gw;
+    const int64_t gbase = ((b * lat + gi * pl) * lon + gj * pw) * chans;
     __syncthreads();
-    for (int64_t f = threadIdx.x; f < F; f += blockDim.x) sdec[(f / PP) * PS + f % PP] = dec_tok[tk * F + f];
+    for (int f = t0; f < F; f += blockDim.x) {
+      const int c = f / PP;
+      sdec[c * PS + (f - c * PP)] = dec_tok[tk * F + f];
+    }
     __syncthreads();
-    for (int64_t e = threadIdx.x; e < F; e += blockDim.x) {
-      const int64_t c = e % chans, j = (e / chans) % pw, i = e / (chans * pw);
-      const int64_t ya = gi * pl + i;
-      const int64_t ga = ((b * lat + ya) * lon + gj * pw + j) * chans + c;
-      const int si = static_cast<int>(c * PS + i * pw + j);
-      const float dec = sdec[si];
-      const float xv = x[ga];
-      const float w = blend_w[c];
-      const float o = w * dec + (1.0f - w) * xv;
-      if (out) out[ga] = o;
-      if (!want_grad) continue;
-      float g;
-      if (g_ext) {
-        g = g_ext[ga];
-      } else {
-        const float wt = lat_w[ya] * var_w[c];
-        const float er = o - target[ga];
-        lsum += wt * er * er;
-        g = 2.0f * wt * er * inv_count * loss_scale;
+    if (active) {
+      for (int e = t0; e < F; e += stride) {
+        const int i = e / RW, r = e - i * RW, j = r / C;  // channel == my_c
+        const int64_t ga = gbase + static_cast<int64_t>(i) * lon * chans + r;
+        const int si = my_c * PS + i * PW + j;
+        const float dec = sdec[si];
+        const float xv = x[ga];
+        const float o = w * dec + (1.0f - w) * xv;
+        if (out) out[ga] = o;
+        if (!want_grad) continue;
+        float g;
+        if (g_ext) {
+          g = g_ext[ga];
+        } else {
+          const float wt = lat_w[gi * pl + i] * vw;
+          const float er = o - target[ga];
+          lsum += wt * er * er;
+          g = 2.0f * wt * er * inv_count * loss_scale;
+        }
+        gb += g * (dec - xv);
+        sgd[si] = g * w;
       }
-      atomicAdd(&s_gb[c], g * (dec - xv));
-      sgd[si] = g * w;
     }
     if (!want_grad) continue;
     __syncthreads();
-    for (int64_t f = threadIdx.x; f < F; f += blockDim.x) {
-      const float gd = sgd[(f / PP) * PS + f % PP];
+    for (int f = t0; f < F; f += blockDim.x) {
+      const int c = f / PP;
+      const float gd = sgd[c * PS + (f - c * PP)];
       if (g_dec_f32) g_dec_f32[tk * F + f] = gd;
       if (g_dec_bf16) g_dec_bf16[tk * F + f] = __float2bfloat16_rn(gd);
     }
   }
   __syncthreads();
+  if (active && want_grad) atomicAdd(&s_gb[my_c], gb);
   lsum = warp_sum(lsum);
   if ((threadIdx.x & 31) == 0) s_loss[threadIdx.x >> 5] = lsum;
   __syncthreads();
@@ -392,7 +410,7 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
     if (threadIdx.x == 0 && loss_sum && target && !g_ext) atomicAdd(loss_sum, v * inv_count);
   }
   if (g_blend && want_grad)
-    for (int c = threadIdx.x; c < chans; c += blockDim.x) atomicAdd(g_blend + c, s_gb[c]);
+    for (int c = t0; c < C; c += blockDim.x) atomicAdd(g_blend + c, s_gb[c]);
 }
 
 // ---------------------------------------------------------------- Adam
@@ -473,32 +491,93 @@ struct EpiArgs {
   float* stats; int64_t stats_bs;
 };
 
-__global__ void epilogue_kernel(const EpiArgs a) {
+__device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t r, int64_t c, float rb, float* v,
+                                           float& s1, float& s2) {
+  if (a.nplanes > 1) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = 0.f;
+    for (int pl = 0; pl < a.nplanes; ++pl) {
+      float t[8];
+      jgd::load8(a.acc, pl * a.a_bs + r * a.lda + c, a.acc_bf16, t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] += t[k];
+    }
+  } else {
+    jgd::load8(a.acc, b * a.a_bs + r * a.lda + c, a.acc_bf16, v);
+  }
+  float t[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = v[k] * a.alpha + rb;
+  if (a.epi & JG_EPI_BIAS_COL) {
+    jgd::load8(a.bias, b * a.bias_bs + c, false, t);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += t[k];
+  }
+  if (a.epi & JG_EPI_RESID) {
+    jgd::load8(a.resid, b * a.r_bs + r * a.ldr + c, false, t);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += t[k];
+  }
+  if (a.epi & JG_EPI_GELU_BWD) {
+    jgd::load8(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16, t);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] *= jgd::gelu_grad_f(t[k]);
+  }
+  const int64_t od = b * a.d_bs + r * a.ldd + c;
+  if (a.epi & JG_EPI_ACCUM) {
+    jgd::load8(a.d, od, false, t);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += t[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    s1 += v[k];
+    s2 += v[k] * v[k];
+  }
+  if (a.d) jgd::store8(a.d, od, a.d_bf16, v);
+  if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
+    if (a.epi & JG_EPI_GELU_FWD) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = jgd::gelu_f(v[k]);
+      jgd::store8(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, t);
+    } else {
+      jgd::store8(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, v);
+    }
+  }
+}
+
+__global__ void epilogue_kernel(const EpiArgs a, bool vec) {
   const int64_t b = blockIdx.y;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < a.m; r += warps) {
     const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
     float s1 = 0.f, s2 = 0.f;
-    for (int64_t c = lane; c < a.n; c += 32) {
-      float v = 0.f;
-      if (a.nplanes > 1) {
-        for (int pl = 0; pl < a.nplanes; ++pl) v += jgd::load1(a.acc, pl * a.a_bs + r * a.lda + c, a.acc_bf16);
-      } else {
-        v = jgd::load1(a.acc, b * a.a_bs + r * a.lda + c, a.acc_bf16);
+    if (vec) {
+      for (int64_t c = lane * 8; c < a.n; c += 256) {
+        float v[8];
+        epi_apply8(a, b, r, c, rb, v, s1, s2);
       }
-      v *= a.alpha;
-      if (a.epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
-      v += rb;
-      if (a.epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
-      if (a.epi & JG_EPI_GELU_BWD) v *= jgd::gelu_grad_f(jgd::load1(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16));
-      const int64_t od = b * a.d_bs + r * a.ldd + c;
-      if (a.epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
-      s1 += v;
-      s2 += v * v;
-      if (a.d) jgd::store1(a.d, od, a.d_bf16, v);
-      if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
-        jgd::store1(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
+    } else {
+      for (int64_t c = lane; c < a.n; c += 32) {
+        float v = 0.f;
+        if (a.nplanes > 1) {
+          for (int pl = 0; pl < a.nplanes; ++pl) v += jgd::load1(a.acc, pl * a.a_bs + r * a.lda + c, a.acc_bf16);
+        } else {
+          v = jgd::load1(a.acc, b * a.a_bs + r * a.lda + c, a.acc_bf16);
+        }
+        v = v * a.alpha + rb;
+        if (a.epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
+        if (a.epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
+        if (a.epi & JG_EPI_GELU_BWD) v *= jgd::gelu_grad_f(jgd::load1(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16));
+        const int64_t od = b * a.d_bs + r * a.ldd + c;
+        if (a.epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
+        s1 += v;
+        s2 += v * v;
+        if (a.d) jgd::store1(a.d, od, a.d_bf16, v);
+        if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
+          jgd::store1(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
+      }
     }
     if (a.epi & JG_EPI_STATS) {
       s1 = warp_sum(s1);
@@ -687,6 +766,7 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
   if (smem > 40 * 1024)
     cudaFuncSetAttribute(blend_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = static_cast<int>(ntok < jg::num_sms() * 4 ? ntok : jg::num_sms() * 4);
+  JG_SHAPE_CHECK(chans <= 256, "jg_blend_loss: at most 256 channels");
   blend_loss_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
       dec_tok, x, target, blend_w, lat_w, var_w, g_out_ext, out, loss_sum, g_blend, g_dec_f32,
       (__nv_bfloat16*)g_dec_bf16, batch, lat, lon, chans, p_lat, p_lon, inv_count, loss_scale);
@@ -739,7 +819,12 @@ int jg_epilogue(const jg_gemm_desc* g, const void* acc, int32_t acc_type, int64_
   a.pre = g->pre; a.ldp = g->ldp; a.p_bs = g->p_bstride; a.pre_bf16 = g->pre_type == JG_BF16;
   a.stats = g->stats; a.stats_bs = g->stats_bstride;
   dim3 grid((unsigned)grid_for(g->m, 8), (unsigned)g->batch);
-  epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  const bool vec = g->n % 8 == 0 && lda % 8 == 0 && acc_bstride % 8 == 0 && g->ldd % 8 == 0 && g->ldd2 % 8 == 0 &&
+                   g->ldr % 8 == 0 && g->ldp % 8 == 0 && g->bias_bstride % 8 == 0 && a16(acc) && a16(g->d) &&
+                   a16(g->d2) && a16(g->bias) && a16(g->resid) && a16(g->pre) && g->d_bstride % 8 == 0 &&
+                   g->r_bstride % 8 == 0 && g->p_bstride % 8 == 0 && g->d2_bstride % 8 == 0;
+  epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a, vec);
   JG_LAUNCH_CHECK("epilogue");
   return JG_OK;
 }
