@@ -57,14 +57,14 @@ struct GemmParams {
   int remote;
 };
 
-template <int BN, bool TF32>
+template <int BN, bool TF32, int CG = 1>
 struct Cfg {
   static constexpr int ESIZE = TF32 ? 4 : 2;
   static constexpr int BK = 128 / ESIZE;           // one 128-byte swizzle atom of K
   static constexpr int UMMA_K = TF32 ? 8 : 16;     // 32 bytes of K per instruction
   static constexpr int ATOM = 128 / ESIZE;         // elements per 128B row of an MN-major box
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = (BN / CG) * 128;  // 2-CTA: each CTA holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;          // double-buffered fp32 accumulator
@@ -75,7 +75,7 @@ struct Cfg {
       | ((TF32 ? 2u : 1u) << 7)                    // A format: tf32 / bf16
       | ((TF32 ? 2u : 1u) << 10)                   // B format
       | (static_cast<uint32_t>(BN >> 3) << 17)     // N
-      | (static_cast<uint32_t>(BM >> 4) << 24);    // M
+      | (static_cast<uint32_t>((BM * CG) >> 4) << 24);  // M (256 for a CTA pair)
 };
 
 // Stage one warp's 32 x 32 accumulator chunk (thread = row) in 128B / 64B-swizzled smem and
@@ -107,9 +107,10 @@ __device__ __forceinline__ void stage_store(uint8_t* stg, const float* v, bool b
   }
 }
 
-template <int BN, bool TF32>
+template <int BN, bool TF32, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
-  using C = Cfg<BN, TF32>;
+  using C = Cfg<BN, TF32, CG>;
+  static_assert(CG == 1 || !TF32, "2-CTA path is bf16 only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -135,15 +136,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     }
     for (int s = 0; s < 2; ++s) {
       jgd::mbar_init(&tfull[s], 1);
-      jgd::mbar_init(&tempty[s], 4);
+      jgd::mbar_init(&tempty[s], 4 * CG);  // every epilogue warp of the pair drains the leader's slot
     }
     jgd::mbar_fence_init();
   }
-  if (warp == 2) jgd::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  const uint32_t cta_rank = CG == 2 ? jgd::cluster_ctarank() : 0;
+  const bool leader = cta_rank == 0;
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      jgd::tmem_alloc_2sm(tmem_slot, C::TMEM_COLS);
+    else
+      jgd::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   jgd::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    jgd::cluster_sync();
+  else
+    __syncthreads();
   jgd::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int tile0 = blockIdx.x / CG, tstep = gridDim.x / CG;
 
   const int kb_batches = p.reduce_batch ? p.batch : 1;
   const int kb_per_tile = p.nseg * kb_batches * p.num_kb;
@@ -153,11 +165,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     // ===================== TMA producer =====================
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
       const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
       const int rem = tile - tb * tiles_per_batch;
-      const int m0 = (rem / p.n_tiles) * BM;
-      const int n0 = (rem % p.n_tiles) * BN;
+      const int m0 = (rem / p.n_tiles) * (BM * CG) + BM * static_cast<int>(cta_rank);
+      const int n0 = (rem % p.n_tiles) * BN + (BN / CG) * static_cast<int>(cta_rank);
       for (int seg = 0; seg < p.nseg; ++seg) {
         for (int bb = 0; bb < kb_batches; ++bb) {
           const int b = p.reduce_batch ? bb : tb;
@@ -165,31 +177,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           const int bbz = p.b_batched ? b : 0;
           for (int kb = 0; kb < p.num_kb; ++kb) {
             jgd::mbar_wait(&empty[stage], phase ^ 1);
-            jgd::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            if (leader) jgd::mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
             const int k0 = kb * C::BK;
             uint8_t* sa = smem_a + stage * C::A_BYTES;
             uint8_t* sb = smem_b + stage * C::B_BYTES;
+            auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, int c2) {
+              if constexpr (CG == 2)
+                jgd::tma_load_3d_2sm(dst, map, &full[stage], c0, c1, c2);
+              else
+                jgd::tma_load_3d(dst, map, &full[stage], c0, c1, c2);
+            };
             if (p.a_mn) {
 #pragma unroll
-              for (int j = 0; j < BM / C::ATOM; ++j)
-                jgd::tma_load_3d(sa + j * (C::BK * 128), &p.tma_a[seg], &full[stage], m0 + j * C::ATOM, k0, ba);
+              for (int j = 0; j < BM / C::ATOM; ++j) load(sa + j * (C::BK * 128), &p.tma_a[seg], m0 + j * C::ATOM, k0, ba);
             } else {
-              jgd::tma_load_3d(sa, &p.tma_a[seg], &full[stage], k0, m0, ba);
+              load(sa, &p.tma_a[seg], k0, m0, ba);
             }
             if (p.b_mn) {
 #pragma unroll
-              for (int j = 0; j < BN / C::ATOM; ++j)
-                jgd::tma_load_3d(sb + j * (C::BK * 128), &p.tma_b[seg], &full[stage], n0 + j * C::ATOM, k0, bbz);
+              for (int j = 0; j < BN / CG / C::ATOM; ++j)
+                load(sb + j * (C::BK * 128), &p.tma_b[seg], n0 + j * C::ATOM, k0, bbz);
             } else {
-              jgd::tma_load_3d(sb, &p.tma_b[seg], &full[stage], k0, n0, bbz);
+              load(sb, &p.tma_b[seg], k0, n0, bbz);
             }
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ===================== MMA issuer =====================
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ===================== MMA issuer (leader CTA of a pair issues for both) =====================
     const uint32_t idesc = C::IDESC_BASE | (static_cast<uint32_t>(p.a_mn) << 15) | (static_cast<uint32_t>(p.b_mn) << 16);
     // K-major: SBO = 8 rows * 128B, per-instruction K step = 32 bytes inside the swizzle atom.
     // MN-major: LBO = one (ATOM x BK) box, SBO = 8 K-rows * 128B, K step = UMMA_K rows * 128B.
@@ -199,7 +216,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
       jgd::mbar_wait(&tempty[acc], acc_phase ^ 1);
       jgd::tc_fence_after();
       const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -212,15 +229,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
         for (int kk = 0; kk < C::BK / C::UMMA_K; ++kk) {
           const uint64_t ad = jgd::make_sdesc(sa + kk * a_kstep, a_lbo, 1024);
           const uint64_t bd = jgd::make_sdesc(sb + kk * b_kstep, b_lbo, 1024);
-          if (TF32)
+          if constexpr (TF32)
             jgd::umma_tf32(d_tmem, ad, bd, idesc, (i | kk) != 0);
+          else if constexpr (CG == 2)
+            jgd::umma_bf16_2sm(d_tmem, ad, bd, idesc, (i | kk) != 0);
           else
             jgd::umma_bf16(d_tmem, ad, bd, idesc, (i | kk) != 0);
         }
-        jgd::umma_commit(&empty[stage]);
+        if constexpr (CG == 2)
+          jgd::umma_commit_2sm(&empty[stage], 0x3);
+        else
+          jgd::umma_commit(&empty[stage]);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
-      jgd::umma_commit(&tfull[acc]);
+      if constexpr (CG == 2)
+        jgd::umma_commit_2sm(&tfull[acc], 0x3);
+      else
+        jgd::umma_commit(&tfull[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
@@ -237,10 +262,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       bc1 = 1.0f / (1.0f - powf(ab1, (float)t));
       bc2 = 1.0f / (1.0f - powf(ab2, (float)t));
     }
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
       const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
       const int rem = tile - tb * tiles_per_batch;
-      const int m0 = (rem / p.n_tiles) * BM;
+      const int m0 = (rem / p.n_tiles) * (BM * CG) + BM * static_cast<int>(cta_rank);
       const int n0 = (rem % p.n_tiles) * BN;
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < p.m;
@@ -448,7 +473,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       }
       jgd::tc_fence_before();
       __syncwarp();
-      if (lane == 0) jgd::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          jgd::mbar_arrive_leader(&tempty[acc]);
+        else
+          jgd::mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) jgd::bulk_wait0();  // every TMA store of this warp has landed
@@ -456,10 +486,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     if (p.remote) __threadfence_system();  // peer stores visible before the group barrier
   }
 
-  __syncthreads();
+  jgd::tc_fence_before();
+  if constexpr (CG == 2)
+    jgd::cluster_sync();  // the leader's MMAs read the peer's smem: nobody leaves early
+  else
+    __syncthreads();
   if (warp == 2) {
     jgd::tc_fence_after();
-    jgd::tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if constexpr (CG == 2)
+      jgd::tmem_dealloc_2sm(tmem_base, C::TMEM_COLS);
+    else
+      jgd::tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -546,18 +583,32 @@ int make_store_map(CUtensorMap* map, void* ptr, bool bf16, int64_t rows, int64_t
   return JG_OK;
 }
 
-template <int BN, bool TF32>
+template <int BN, bool TF32, int CG>
 int launch(GemmParams& p, cudaStream_t stream) {
-  using C = Cfg<BN, TF32>;
+  using C = Cfg<BN, TF32, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, TF32, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return jg::cuda_check(attr_err, "cudaFuncSetAttribute(gemm)");
-  const int grid = p.num_tiles < jg::num_sms() ? p.num_tiles : jg::num_sms();
-  gemm_kernel<BN, TF32><<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(p);
+  const int max_units = jg::num_sms() / CG;
+  const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, TF32, CG>, p);
+  if (e != cudaSuccess) return jg::cuda_check(e, "gemm_kernel launch");
   JG_LAUNCH_CHECK("gemm_kernel");
   return JG_OK;
 }
@@ -623,15 +674,18 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   const int bk = 128 / esize;
   p.num_kb = static_cast<int>((g->k + bk - 1) / bk);
 
-  // tile width: the widest N tile that still gives at least one full wave of tiles
+  // tile width: the widest N tile that still gives at least one full wave of tiles; bf16 problems
+  // taller than one 128-row tile run on CTA pairs (cta_group::2, 256-row tiles, B split in two).
   const int64_t out_batches = p.reduce_batch ? 1 : g->batch;
-  const int64_t mt = (g->m + BM - 1) / BM;
+  static const bool no_2sm = getenv("JG_NO_2SM") != nullptr;
+  const int cg = (!tf32 && g->m > BM && g->n > 64 && !no_2sm) ? 2 : 1;
+  const int64_t mt = (g->m + BM * cg - 1) / (BM * cg);
   int bn = 256;
   if (g->n <= 64) bn = 64;
   else if (g->n <= 128) bn = 128;
   else {
     const int64_t t256 = mt * ((g->n + 255) / 256) * out_batches;
-    if (t256 < jg::num_sms()) bn = 128;
+    if (t256 < jg::num_sms() / cg) bn = 128;
   }
   p.m_tiles = static_cast<int>(mt);
   p.n_tiles = static_cast<int>((g->n + bn - 1) / bn);
@@ -647,7 +701,7 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
                               p.a_batched ? g->batch : 1, BM);
     if (rc) return rc;
     rc = make_operand_map(&p.tma_b[s], bs[s], tf32, p.b_mn, g->n, g->k, g->ldb, g->b_bstride,
-                          p.b_batched ? g->batch : 1, bn);
+                          p.b_batched ? g->batch : 1, bn / cg);
     if (rc) return rc;
   }
 
@@ -689,11 +743,15 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   }
 
   if (tf32) {
-    if (bn == 256) return launch<256, true>(p, stream);
-    if (bn == 128) return launch<128, true>(p, stream);
-    return launch<64, true>(p, stream);
+    if (bn == 256) return launch<256, true, 1>(p, stream);
+    if (bn == 128) return launch<128, true, 1>(p, stream);
+    return launch<64, true, 1>(p, stream);
   }
-  if (bn == 256) return launch<256, false>(p, stream);
-  if (bn == 128) return launch<128, false>(p, stream);
-  return launch<64, false>(p, stream);
+  if (cg == 2) {
+    if (bn == 256) return launch<256, false, 2>(p, stream);
+    return launch<128, false, 2>(p, stream);
+  }
+  if (bn == 256) return launch<256, false, 1>(p, stream);
+  if (bn == 128) return launch<128, false, 1>(p, stream);
+  return launch<64, false, 1>(p, stream);
 }
