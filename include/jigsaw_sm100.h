@@ -55,6 +55,14 @@ extern "C" {
                                in place (m, v, bf16 copy alongside) instead of storing the gradient
                                (fused into the producer; no gradient round trip) */
 
+/* Extra destinations of an output (the same element offsets relative to each base): used to
+ * push a Jigsaw all-gather operand straight from its producer into the peers' NVLink-mapped
+ * gather slots, so the gather overlaps the producing kernel. NULL / n = 0: none. */
+typedef struct jg_bcast {
+  void* ptr[4];
+  int32_t n;
+} jg_bcast;
+
 /*
  * jg_gemm — one (batched) GEMM with a fused epilogue.
  * Replaces tensor.matmul (tensor.py:59-72) as called by MpContext._mm (parallel.py:65-69),
@@ -95,6 +103,8 @@ typedef struct jg_gemm_desc {
    * non-NULL, batch b of D is written at d_planes[b] (row stride ldd) — typically a peer GPU's
    * symmetric buffer reached over NVLink — and the epilogue ends with a system-scope fence. */
   void* d_planes[8];
+  /* extra destinations of D and D2 (TMA-store epilogue only; same ld / batch stride) */
+  jg_bcast d_bcast, d2_bcast;
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);
@@ -108,7 +118,7 @@ int jg_gemm(const jg_gemm_desc* desc, void* stream);
  * With nplanes == 1 and desc->batch > 1, acc_bstride is the batch stride instead.
  */
 int jg_epilogue(const jg_gemm_desc* desc, const void* acc, int32_t acc_type, int64_t lda, int64_t acc_bstride,
-                int32_t nplanes, void* stream);
+                int32_t nplanes, void* stream);   /* honours desc->d_bcast / d2_bcast */
 
 /* y += alpha * x (fp32): accumulate a reduce-scattered weight gradient (parallel.py:490-493). */
 int jg_axpy(float* y, const float* x, float alpha, int64_t n, void* stream);
@@ -150,7 +160,7 @@ int jg_ln_moments(const float* x, float* stats, int64_t rows, int64_t cols, int6
 /* phase 1 (forward): y = gamma * (x - mean) * inv_std + beta ; saves (mean, inv_std) per row. */
 int jg_ln_apply(const float* x, const float* stats, const float* gamma, const float* beta,
                 void* y, int32_t y_type, float* mean_rstd, int64_t rows, int64_t cols,
-                int64_t c_total, float eps, void* stream);
+                int64_t c_total, float eps, const jg_bcast* y_bcast, void* stream);
 /* backward phase 0: bstats[r] += (sum h, sum h*xhat) with h = g*gamma, xhat from x & mean_rstd. */
 int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const float* mean_rstd,
                       float* bstats, int64_t rows, int64_t cols, void* stream);
@@ -160,7 +170,7 @@ int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const 
 int jg_ln_bwd_apply(const float* x, const float* g, const float* gamma, const float* mean_rstd,
                     const float* bstats, const float* resid, float* out, void* out_bf16,
                     float* dgamma, float* dbeta, float* rowsum_out,
-                    int64_t rows, int64_t cols, int64_t c_total, void* stream);
+                    int64_t rows, int64_t cols, int64_t c_total, const jg_bcast* op_bcast, void* stream);
 
 /* Column sums (bias gradients, parallel.py:548,559-561): out[c] += sum_r x[r*ld + c];
  * Row sums (row-bias gradient of weight-first tok2, parallel.py:536): out[r] += sum_c x[r*ld+c]. */
@@ -191,7 +201,7 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
                   const float* lat_w, const float* var_w, const float* g_out_ext,
                   float* out, float* loss_sum, float* g_blend, float* g_dec_f32, void* g_dec_bf16,
                   int64_t batch, int64_t lat, int64_t lon, int64_t chans, int64_t p_lat, int64_t p_lon,
-                  float inv_count, float loss_scale, void* stream);
+                  float inv_count, float loss_scale, const jg_bcast* gdec_bcast, void* stream);
 
 /*
  * Fused Adam over one flat fp32 parameter range (bias-corrected,

@@ -38,6 +38,23 @@ EXPORTED = [
 ]
 
 
+class Bcast(ctypes.Structure):
+    """jg_bcast: up to 4 extra destinations of an output (peer gather slots)."""
+    _fields_ = [("ptr", ctypes.c_void_p * 4), ("n", ctypes.c_int32)]
+
+
+def make_bcast(addrs) -> "Bcast | None":
+    if not addrs:
+        return None
+    if len(addrs) > 4:
+        raise ValueError("at most 4 broadcast destinations")
+    b = Bcast()
+    for i, a in enumerate(addrs):
+        b.ptr[i] = a
+    b.n = len(addrs)
+    return b
+
+
 class GemmDesc(ctypes.Structure):
     _fields_ = [
         ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("k", ctypes.c_int64), ("batch", ctypes.c_int64),
@@ -57,6 +74,7 @@ class GemmDesc(ctypes.Structure):
         ("adam_step", ctypes.c_void_p), ("adam_lr", ctypes.c_float), ("adam_beta1", ctypes.c_float),
         ("adam_beta2", ctypes.c_float), ("adam_eps", ctypes.c_float),
         ("d_planes", ctypes.c_void_p * 8),
+        ("d_bcast", Bcast), ("d2_bcast", Bcast),
     ]
 
 
@@ -83,14 +101,14 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_gelu_fwd": [vp, vp, i32, i64, vp],
         "jg_gelu_bwd": [vp, vp, vp, i32, i64, vp],
         "jg_ln_moments": [vp, vp, i64, i64, i64, vp],
-        "jg_ln_apply": [vp, vp, vp, vp, vp, i32, vp, i64, i64, i64, f32, vp],
+        "jg_ln_apply": [vp, vp, vp, vp, vp, i32, vp, i64, i64, i64, f32, vp, vp],
         "jg_ln_bwd_moments": [vp, vp, vp, vp, vp, i64, i64, vp],
-        "jg_ln_bwd_apply": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, vp],
+        "jg_ln_bwd_apply": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, vp, vp],
         "jg_colsum": [vp, i32, vp, i64, i64, i64, vp],
         "jg_rowsum": [vp, i32, vp, i64, i64, i64, vp],
         "jg_patchify": [vp, vp, i32, i64, i64, i64, i64, i64, i64, vp],
         "jg_unpatchify": [vp, vp, i64, i64, i64, i64, i64, i64, vp],
-        "jg_blend_loss": [vp] * 12 + [i64] * 6 + [f32, f32, vp],
+        "jg_blend_loss": [vp] * 12 + [i64] * 6 + [f32, f32, vp, vp],
         "jg_adam": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp],
         "jg_step_increment": [vp, vp],
         "jg_sqnorm": [vp, i64, vp, vp],

@@ -32,6 +32,9 @@ struct GemmParams {
   CUtensorMap tma_b[3];
   CUtensorMap tma_d[8];   // D store maps: [0] = batched D, or one per remote output plane
   CUtensorMap tma_d2;
+  CUtensorMap tma_dx[4];  // extra destinations (peer gather slots) of D and of D2
+  CUtensorMap tma_d2x[4];
+  int nb_d, nb_d2;
   int tma_store;          // 1: epilogue writes D / D2 through TMA bulk tensor stores
   int nseg;
   int m, n, k;
@@ -81,7 +84,8 @@ struct Cfg {
 // Stage one warp's 32 x 32 accumulator chunk (thread = row) in 128B / 64B-swizzled smem and
 // TMA-store it: rows become contiguous bulk writes (HBM or an NVLink peer), conflict-free smem.
 __device__ __forceinline__ void stage_store(uint8_t* stg, const float* v, bool bf16, int lane,
-                                            const CUtensorMap* map, int c0, int c1, int c2) {
+                                            const CUtensorMap* map, int c0, int c1, int c2,
+                                            const CUtensorMap* extra = nullptr, int n_extra = 0) {
   if (lane == 0) jgd::bulk_wait_read0();
   __syncwarp();
   if (bf16) {
@@ -103,6 +107,7 @@ __device__ __forceinline__ void stage_store(uint8_t* stg, const float* v, bool b
   __syncwarp();
   if (lane == 0) {
     jgd::tma_store_3d(map, stg, c0, c1, c2);
+    for (int i = 0; i < n_extra; ++i) jgd::tma_store_3d(extra + i, stg, c0, c1, c2);  // same tile, peers
     jgd::bulk_commit();
   }
 }
@@ -430,13 +435,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           // stage the warp's 32 x 32 chunk in swizzled smem, one TMA bulk tensor store per output
           const int rbase = m0 + q * 32;
           if (p.remote || p.d != nullptr)
-            stage_store(stg, v, p.d_bf16, lane, &p.tma_d[p.remote ? tb : 0], col0, rbase, p.remote ? 0 : tb);
+            stage_store(stg, v, p.d_bf16, lane, &p.tma_d[p.remote ? tb : 0], col0, rbase, p.remote ? 0 : tb,
+                        p.tma_dx, p.nb_d);
           if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
             if (epi & JG_EPI_GELU_FWD) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = jgd::gelu_f(v[j]);
             }
-            stage_store(stg, v, p.d2_bf16, lane, &p.tma_d2, col0, rbase, tb);
+            stage_store(stg, v, p.d2_bf16, lane, &p.tma_d2, col0, rbase, tb, p.tma_d2x, p.nb_d2);
           }
           continue;
         }
@@ -740,7 +746,22 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
       int rc = make_store_map(&p.tma_d2, g->d2, g->d2_type == JG_BF16, g->m, g->n, g->ldd2, g->d2_bstride, out_batches);
       if (rc) return rc;
     }
+    p.nb_d = p.remote ? 0 : g->d_bcast.n;
+    p.nb_d2 = (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) ? g->d2_bcast.n : 0;
+    JG_SHAPE_CHECK(p.nb_d >= 0 && p.nb_d <= 4 && p.nb_d2 >= 0 && p.nb_d2 <= 4, "jg_gemm: at most 4 broadcast targets");
+    for (int i = 0; i < p.nb_d; ++i) {
+      int rc = make_store_map(&p.tma_dx[i], g->d_bcast.ptr[i], dbf, g->m, g->n, g->ldd, g->d_bstride, out_batches);
+      if (rc) return rc;
+    }
+    for (int i = 0; i < p.nb_d2; ++i) {
+      int rc = make_store_map(&p.tma_d2x[i], g->d2_bcast.ptr[i], g->d2_type == JG_BF16, g->m, g->n, g->ldd2,
+                              g->d2_bstride, out_batches);
+      if (rc) return rc;
+    }
+  } else {
+    JG_SHAPE_CHECK(g->d_bcast.n == 0 && g->d2_bcast.n == 0, "jg_gemm: broadcast outputs need a write-only D");
   }
+  if (p.nb_d || p.nb_d2) p.remote = 1;  // system fence at the end: peers read after the barrier
 
   if (tf32) {
     if (bn == 256) return launch<256, true, 1>(p, stream);

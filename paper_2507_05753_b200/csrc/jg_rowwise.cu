@@ -8,6 +8,27 @@ namespace {
 
 using jgd::warp_sum;
 
+struct Bcast {
+  void* p[4];
+  int n;
+};
+Bcast to_bcast(const jg_bcast* b) {
+  Bcast o{};
+  if (b) {
+    o.n = b->n < 4 ? b->n : 4;
+    for (int i = 0; i < o.n; ++i) o.p[i] = b->ptr[i];
+  }
+  return o;
+}
+__device__ __forceinline__ void store8_bc(void* base, const Bcast& bc, int64_t off, bool bf16, const float* v) {
+  jgd::store8(base, off, bf16, v);
+  for (int i = 0; i < bc.n; ++i) jgd::store8(bc.p[i], off, bf16, v);
+}
+__device__ __forceinline__ void store1_bc(void* base, const Bcast& bc, int64_t off, bool bf16, float v) {
+  jgd::store1(base, off, bf16, v);
+  for (int i = 0; i < bc.n; ++i) jgd::store1(bc.p[i], off, bf16, v);
+}
+
 int grid_for(int64_t work_items, int per_block) {
   int64_t b = (work_items + per_block - 1) / per_block;
   const int64_t cap = static_cast<int64_t>(jg::num_sms()) * 16;
@@ -122,7 +143,7 @@ __global__ void ln_moments_kernel(const float* __restrict__ x, float* __restrict
 __global__ void ln_apply_kernel(const float* __restrict__ x, const float* __restrict__ stats,
                                 const float* __restrict__ gamma, const float* __restrict__ beta, void* __restrict__ y,
                                 bool y_bf16, float* __restrict__ mean_rstd, int64_t rows, int64_t cols,
-                                float inv_ctotal, float eps) {
+                                float inv_ctotal, float eps, const Bcast bc) {
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   const bool vec = (cols % 8 == 0);
@@ -144,13 +165,14 @@ __global__ void ln_apply_kernel(const float* __restrict__ x, const float* __rest
         jgd::load8(beta, c, false, bt);
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = gm[j] * ((v[j] - mean) * rstd) + bt[j];
-        jgd::store8(y, yo + c, y_bf16, v);
+        store8_bc(y, bc, yo + c, y_bf16, v);
       }
     } else {
       for (int64_t c = lane; c < cols; c += 32)
-        jgd::store1(y, yo + c, y_bf16, gamma[c] * ((xr[c] - mean) * rstd) + beta[c]);
+        store1_bc(y, bc, yo + c, y_bf16, gamma[c] * ((xr[c] - mean) * rstd) + beta[c]);
     }
   }
+  if (bc.n) __threadfence_system();  // peer copies complete before the group barrier
 }
 
 __global__ void ln_bwd_moments_kernel(const float* __restrict__ x, const float* __restrict__ g,
@@ -201,7 +223,7 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
                                     const float* __restrict__ bstats, const float* __restrict__ resid,
                                     float* __restrict__ out, __nv_bfloat16* __restrict__ out_bf16,
                                     float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows, int64_t cols,
-                                    float inv_ctotal) {
+                                    float inv_ctotal, const Bcast bc) {
   const int64_t c0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
   const int64_t r0 = blockIdx.y * (int64_t)LNB_ROWS;
   if (c0 >= cols) return;
@@ -246,11 +268,15 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
         raw.x = *reinterpret_cast<uint32_t*>(&lo);
         raw.y = *reinterpret_cast<uint32_t*>(&hi);
         *reinterpret_cast<uint2*>(out_bf16 + o) = raw;
+        for (int i = 0; i < bc.n; ++i) *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(bc.p[i]) + o) = raw;
       }
     } else {
       for (int j = 0; j < nc; ++j) {
         out[o + j] = ov[j];
-        if (out_bf16) out_bf16[o + j] = __float2bfloat16_rn(ov[j]);
+        if (out_bf16) {
+          out_bf16[o + j] = __float2bfloat16_rn(ov[j]);
+          for (int i = 0; i < bc.n; ++i) reinterpret_cast<__nv_bfloat16*>(bc.p[i])[o + j] = __float2bfloat16_rn(ov[j]);
+        }
       }
     }
   }
@@ -258,6 +284,7 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
     if (dgamma) atomicAdd(dgamma + c0 + j, dg[j]);
     if (dbeta) atomicAdd(dbeta + c0 + j, db[j]);
   }
+  if (bc.n) __threadfence_system();
 }
 
 // ---------------------------------------------------------------- bias-grad reductions
@@ -341,7 +368,8 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
                                   const float* __restrict__ g_ext, float* __restrict__ out, float* __restrict__ loss_sum,
                                   float* __restrict__ g_blend, float* __restrict__ g_dec_f32,
                                   __nv_bfloat16* __restrict__ g_dec_bf16, int64_t batch, int64_t lat, int64_t lon,
-                                  int64_t chans, int64_t pl, int64_t pw, float inv_count, float loss_scale) {
+                                  int64_t chans, int64_t pl, int64_t pw, float inv_count, float loss_scale,
+                                  const Bcast bc) {
   extern __shared__ float sm[];
   __shared__ float s_gb[MAX_CH];
   __shared__ float s_loss[32];
@@ -395,8 +423,8 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
     for (int f = t0; f < F; f += blockDim.x) {
       const int c = f / PP;
       const float gd = sgd[c * PS + (f - c * PP)];
-      if (g_dec_f32) g_dec_f32[tk * F + f] = gd;
-      if (g_dec_bf16) g_dec_bf16[tk * F + f] = __float2bfloat16_rn(gd);
+      if (g_dec_f32) store1_bc(g_dec_f32, bc, tk * F + f, false, gd);
+      if (g_dec_bf16) store1_bc(g_dec_bf16, bc, tk * F + f, true, gd);
     }
   }
   __syncthreads();
@@ -411,6 +439,7 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
   }
   if (g_blend && want_grad)
     for (int c = t0; c < C; c += blockDim.x) atomicAdd(g_blend + c, s_gb[c]);
+  if (bc.n) __threadfence_system();
 }
 
 // ---------------------------------------------------------------- Adam
@@ -489,6 +518,7 @@ struct EpiArgs {
   const float* resid; int64_t ldr, r_bs;
   const void* pre; int64_t ldp, p_bs; bool pre_bf16;
   float* stats; int64_t stats_bs;
+  Bcast dbc, d2bc;
 };
 
 __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t r, int64_t c, float rb, float* v,
@@ -534,14 +564,14 @@ __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t 
     s1 += v[k];
     s2 += v[k] * v[k];
   }
-  if (a.d) jgd::store8(a.d, od, a.d_bf16, v);
+  if (a.d) store8_bc(a.d, a.dbc, od, a.d_bf16, v);
   if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
     if (a.epi & JG_EPI_GELU_FWD) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) t[k] = jgd::gelu_f(v[k]);
-      jgd::store8(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, t);
+      store8_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, t);
     } else {
-      jgd::store8(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, v);
+      store8_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, v);
     }
   }
 }
@@ -574,9 +604,9 @@ __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
         if (a.epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
         s1 += v;
         s2 += v * v;
-        if (a.d) jgd::store1(a.d, od, a.d_bf16, v);
+        if (a.d) store1_bc(a.d, a.dbc, od, a.d_bf16, v);
         if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
-          jgd::store1(a.d2, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
+          store1_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
       }
     }
     if (a.epi & JG_EPI_STATS) {
@@ -588,6 +618,7 @@ __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
       }
     }
   }
+  if (a.dbc.n || a.d2bc.n) __threadfence_system();
 }
 
 __global__ void sum_planes_kernel(float* __restrict__ y, const float* __restrict__ x, int64_t n, int nplanes,
@@ -667,13 +698,15 @@ int jg_ln_moments(const float* x, float* stats, int64_t rows, int64_t cols, int6
 }
 
 int jg_ln_apply(const float* x, const float* stats, const float* gamma, const float* beta, void* y, int32_t y_type,
-                float* mean_rstd, int64_t rows, int64_t cols, int64_t c_total, float eps, void* stream) {
+                float* mean_rstd, int64_t rows, int64_t cols, int64_t c_total, float eps, const jg_bcast* y_bcast,
+                void* stream) {
   JG_SHAPE_CHECK(eps > 0.f, "layer_norm eps must be > 0, got %g", (double)eps);
   JG_SHAPE_CHECK(rows >= 0 && cols > 0 && c_total >= cols, "jg_ln_apply: bad shape");
   JG_SHAPE_CHECK(al16(x) && al16(y) && al16(gamma) && al16(beta), "jg_ln_apply: pointers must be 16B aligned");
   if (rows == 0) return JG_OK;
   ln_apply_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(x, stats, gamma, beta, y, y_type == JG_BF16,
-                                                                      mean_rstd, rows, cols, 1.0f / (float)c_total, eps);
+                                                                      mean_rstd, rows, cols, 1.0f / (float)c_total, eps,
+                                                                      to_bcast(y_bcast));
   JG_LAUNCH_CHECK("ln_apply");
   return JG_OK;
 }
@@ -690,14 +723,14 @@ int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const 
 
 int jg_ln_bwd_apply(const float* x, const float* g, const float* gamma, const float* mean_rstd, const float* bstats,
                     const float* resid, float* out, void* out_bf16, float* dgamma, float* dbeta, float* rowsum_out,
-                    int64_t rows, int64_t cols, int64_t c_total, void* stream) {
+                    int64_t rows, int64_t cols, int64_t c_total, const jg_bcast* op_bcast, void* stream) {
   JG_SHAPE_CHECK(rows >= 0 && cols > 0 && c_total >= cols, "jg_ln_bwd_apply: bad shape");
   JG_SHAPE_CHECK(al16(x) && al16(g) && al16(out) && (!resid || al16(resid)), "jg_ln_bwd_apply: pointers must be 16B aligned");
   if (rows == 0) return JG_OK;
   dim3 grid((unsigned)((cols + 1023) / 1024), (unsigned)((rows + LNB_ROWS - 1) / LNB_ROWS));
   ln_bwd_apply_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, g, gamma, mean_rstd, bstats, resid, out,
                                                                (__nv_bfloat16*)out_bf16, dgamma, dbeta, rows, cols,
-                                                               1.0f / (float)c_total);
+                                                               1.0f / (float)c_total, to_bcast(op_bcast));
   JG_LAUNCH_CHECK("ln_bwd_apply");
   if (rowsum_out) {
     rowsum_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(out, false, rowsum_out, rows, cols, cols);
@@ -755,7 +788,8 @@ int jg_unpatchify(const float* tokens, float* x, int64_t batch, int64_t lat, int
 int jg_blend_loss(const float* dec_tok, const float* x, const float* target, const float* blend_w, const float* lat_w,
                   const float* var_w, const float* g_out_ext, float* out, float* loss_sum, float* g_blend,
                   float* g_dec_f32, void* g_dec_bf16, int64_t batch, int64_t lat, int64_t lon, int64_t chans,
-                  int64_t p_lat, int64_t p_lon, float inv_count, float loss_scale, void* stream) {
+                  int64_t p_lat, int64_t p_lon, float inv_count, float loss_scale, const jg_bcast* gdec_bcast,
+                  void* stream) {
   JG_SHAPE_CHECK(chans <= MAX_CH, "jg_blend_loss: at most %d channels", MAX_CH);
   JG_SHAPE_CHECK(lat % p_lat == 0 && lon % p_lon == 0, "jg_blend_loss: grid not divisible by patch");
   JG_SHAPE_CHECK(!target || (lat_w && var_w), "jg_blend_loss: a target needs lat/var weights");
@@ -769,7 +803,7 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
   JG_SHAPE_CHECK(chans <= 256, "jg_blend_loss: at most 256 channels");
   blend_loss_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
       dec_tok, x, target, blend_w, lat_w, var_w, g_out_ext, out, loss_sum, g_blend, g_dec_f32,
-      (__nv_bfloat16*)g_dec_bf16, batch, lat, lon, chans, p_lat, p_lon, inv_count, loss_scale);
+      (__nv_bfloat16*)g_dec_bf16, batch, lat, lon, chans, p_lat, p_lon, inv_count, loss_scale, to_bcast(gdec_bcast));
   JG_LAUNCH_CHECK("blend_loss");
   return JG_OK;
 }
@@ -818,6 +852,8 @@ int jg_epilogue(const jg_gemm_desc* g, const void* acc, int32_t acc_type, int64_
   a.resid = g->resid; a.ldr = g->ldr; a.r_bs = g->r_bstride;
   a.pre = g->pre; a.ldp = g->ldp; a.p_bs = g->p_bstride; a.pre_bf16 = g->pre_type == JG_BF16;
   a.stats = g->stats; a.stats_bs = g->stats_bstride;
+  a.dbc = to_bcast(&g->d_bcast);
+  a.d2bc = to_bcast(&g->d2_bcast);
   dim3 grid((unsigned)grid_for(g->m, 8), (unsigned)g->batch);
   auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   const bool vec = g->n % 8 == 0 && lda % 8 == 0 && acc_bstride % 8 == 0 && g->ldd % 8 == 0 && g->ldd2 % 8 == 0 &&

@@ -68,10 +68,11 @@ class GridWorkspace:
         self.q = max(1, R // C)  # column-group owner chunks per row-gathered plane
         panel_shape = {"enc.w": (E, Fl), "ch1.w": (H, El), "ch2.w": (E, Hl), "dec.w": (F, El)}
         self.panel_names = [n for n in m.params if _base(n) in CHANNEL_LAYERS] if R > 1 else []
-        row_persist = [(f"u_row{j}", (B, C, Tl, El), od) for j in range(nj)]
+        row_persist = [(f"u_row{j}", (C, B, Tl, El), od) for j in range(nj)]  # plane-major: LN writes its plane
         col_persist = []
         if R > 1:
             col_persist += [(f"a_col{j}", (B, R, Er, Kl), od) for j in range(nj)]
+            col_persist += [("gh_col", (B, R, Er, Kl), od)]
             col_persist += [(f"panel:{n}", (R, panel_shape[_base(n)][0] // R, panel_shape[_base(n)][1]), od)
                             for n in self.panel_names]
         es, ps = torch.empty((), dtype=od).element_size(), 4
@@ -134,12 +135,14 @@ def chan_fwd(m, g, X, panel, M, kin_l, nout, **epi):
     K.epilogue(acc, M, nl, acc_bs=ps, nplanes=npl, **epi)
 
 
-def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None, **dx_epi):
-    """Backward of Y = X W^T: dX (optional, fused epilogue), dW via RS over the column group,
-    bias-gradient partial (summed over the column group in grad_sync)."""
+def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None, dyrow=None, **dx_epi):
+    """Backward of Y = X W^T: dX (optional, fused epilogue, may push its output to peers), dW via
+    RS over the column group, bias-gradient partial (summed over the column group in grad_sync).
+    `dyrow`: dY already gathered over the row group by its producer ([C, M, nout/C])."""
     R, C = m.R, m.C
     nl = nout // C
-    dyrow = g.row.ag(dY)                                        # [C, M, nl]
+    if dyrow is None:
+        dyrow = g.row.ag(dY)                                    # [C, M, nl]
     if dX is not None:
         K.gemm(dX, dyrow, panel, KM, MN, M, kin_l, nl, C, M * nl, nl * kin_l, reduce_batch=True, **dx_epi)
     if R == 1:
@@ -158,31 +161,35 @@ def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None
 
 
 # --------------------------------------------------------------------------- token layers
-def tok1_fwd(m, g, ws, j, bi, b):
-    """h = u^T W1 + b1, a = gelu(h): rows of h (E) gathered over the row group, split R ways."""
+def tok1_fwd(m, g, ws, j, bi, b, urow):
+    """h = u^T W1 + b1, a = gelu(h): rows of h (E) gathered over the row group, split R ways.
+    urow: [C, Tl, El] view of the gathered u (plane stride B*Tl*El). Returns gelu(h) columns
+    gathered over the column group ([E, Kl]) when R > 1, else the local a."""
     p, R, C = m.params, m.R, m.C
-    Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
-    urow = g.row.ag(ws.u[j][bi], slot=f"u_row{j}", sub=bi, nsub=ws.B)  # [C, Tl, El]
+    Tl, El, Er, Kl, B = ws.Tl, ws.El, ws.Er, ws.Kl, ws.B
+    ps = B * Tl * El
     if R == 1:
-        K.gemm(ws.h[j][bi], urow, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
+        K.gemm(ws.h[j][bi], urow, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C, ps, 0, d_bs=El * Kl,
                epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d2=ws.a[j][bi], d2_bs=El * Kl)
-        return
+        return ws.a[j][bi]
     q = g.q
 
     def fn(s, D, d_bs, dpl):  # rows [s*Er, (s+1)*Er) of plane j -> owner j*q+s
-        K.gemm(D, urow[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C, Tl * El, 0, d_bs=d_bs,
+        K.gemm(D, urow[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
                d_planes=dpl, lda=El)
 
-    acc, npl, ps = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
-    K.epilogue(acc, Er, Kl, acc_bs=ps, nplanes=npl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data,
-               d=ws.h[j][bi], d2=ws.a[j][bi])
+    acc, npl, pst = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
+    ha = g.col.dest((Er, Kl), m.op_dtype, slot=f"a_col{j}", sub=bi, nsub=B)   # gelu(h) pushed to peers
+    K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data,
+               d=ws.h[j][bi], d2=ha.own, d2_bcast=ha.peers)
+    g.col.publish(ha)
+    return ha.planes.view(-1, Kl)
 
 
-def tok2_fwd(m, g, ws, j, bi, b):
+def tok2_fwd(m, g, ws, j, bi, b, acol):
     """x2 = x + W2 a^T + b2[:, None]: a gathered over the column group; RS over the row group."""
-    p, R, C = m.params, m.R, m.C
+    p, C = m.params, m.C
     Tl, El, Kl = ws.Tl, ws.El, ws.Kl
-    acol = g.col.ag(ws.a[j][bi], slot=f"a_col{j}", sub=bi, nsub=ws.B).view(-1, Kl) if R > 1 else ws.a[j][bi]
 
     def fn(s, D, d_bs, dpl):
         K.gemm(D, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
@@ -192,34 +199,39 @@ def tok2_fwd(m, g, ws, j, bi, b):
                resid=ws.res[j][bi], d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
 
 
-def tok2_bwd(m, g, ws, j, bi, b):
-    """gh = (g_x2^T W2) * gelu'(h) (RS over the column group); dW2 += g_x2 a (local)."""
+def tok2_bwd(m, g, ws, j, bi, b, grow, acol):
+    """gh = (g_x2^T W2) * gelu'(h) (RS over the column group, pushed back out over it for tok1's
+    backward); dW2 += g_x2 a (local). grow: gathered g_x2 [C, Tl, El] (plane stride B*Tl*El).
+    Returns (gh local block, gh gathered over the column group [E, Kl])."""
     p, R, C = m.params, m.R, m.C
     Tl, El, Er, Kl, B = ws.Tl, ws.El, ws.Er, ws.Kl, ws.B
-    grow = g.row.ag(ws.gx2_op[bi])                              # [C, Tl, El]
-    acol = (g.col.persistent(f"a_col{j}").view(B, -1, Kl)[bi] if R > 1 else ws.a[j][bi])
+    ps = B * Tl * El
     if R == 1:
-        K.gemm(ws.gh[bi], grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, Tl * El, 0, d_bs=El * Kl,
+        K.gemm(ws.gh[bi], grow, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, ps, 0, d_bs=El * Kl,
                epi=E_GB, pre=ws.h[j][bi])
+        gh_local, ghcol = ws.gh[bi], ws.gh[bi]
     else:
         q = g.q
 
         def fn(s, D, d_bs, dpl):
-            K.gemm(D, grow[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C, Tl * El, 0, d_bs=d_bs,
+            K.gemm(D, grow[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
                    d_planes=dpl, lda=El)
 
-        acc, npl, ps = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
-        K.epilogue(acc, Er, Kl, acc_bs=ps, nplanes=npl, epi=E_GB, pre=ws.h[j][bi], d=ws.gh[bi])
+        acc, npl, pst = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
+        hg = g.col.dest((Er, Kl), m.op_dtype, slot="gh_col", sub=bi, nsub=B)
+        K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_GB, pre=ws.h[j][bi], d=hg.own, d_bcast=hg.peers)
+        g.col.publish(hg)
+        gh_local, ghcol = hg.own, hg.planes.view(-1, Kl)
     K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
     out, kw = m._wgrad(b + "tok2.w") if B == 1 else (p[b + "tok2.w"].grad, {"epi": E_ACC})
-    K.gemm(out, grow, acol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
+    K.gemm(out, grow, acol, KM, MN, Tl, Kl, El, C, ps, El * Kl, reduce_batch=True, **kw)
+    return gh_local, ghcol
 
 
-def tok1_bwd(m, g, ws, j, bi, b):
+def tok1_bwd(m, g, ws, j, bi, b, ghcol):
     """gu = W1 gh^T (gh gathered over the column group, RS over the row group); dW1 += u gh."""
-    p, R, C = m.params, m.R, m.C
+    p, C = m.params, m.C
     Tl, El, Kl, B = ws.Tl, ws.El, ws.Kl, ws.B
-    ghcol = g.col.ag(ws.gh[bi]).view(-1, Kl) if R > 1 else ws.gh[bi]
 
     def fn(s, D, d_bs, dpl):
         K.gemm(D, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
@@ -227,20 +239,22 @@ def tok1_bwd(m, g, ws, j, bi, b):
     acc, npl, ps = g.row.rs_gemm(Tl, El, F32, fn, out=ws.gu[bi])
     if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
         K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
-    urow = g.row.persistent(f"u_row{j}").view(B, C, Tl, El)[bi]
+    urow = g.row.persistent(f"u_row{j}").view(C, B, Tl, El)[:, bi]
     out, kw = m._wgrad(b + "tok1.w") if B == 1 else (p[b + "tok1.w"].grad, {"epi": E_ACC})
-    K.gemm(out, urow, ghcol, KM, MN, Tl, Kl, El, C, Tl * El, El * Kl, reduce_batch=True, **kw)
+    K.gemm(out, urow, ghcol, KM, MN, Tl, Kl, El, C, B * Tl * El, El * Kl, reduce_batch=True, **kw)
 
 
 # --------------------------------------------------------------------------- forward / backward
 def forward_grid(m, ws) -> None:
     g = _gw(m, ws)
     cfg, p, ctx = m.cfg, m.params, m.ctx
+    R, C = m.R, m.C
     B = ws.B
     E, H, F = cfg.d_emb, cfg.d_ch, cfg.patch_features
-    Tl, El, Hl, Fl = ws.Tl, ws.El, ws.Hl, ws.Fl
+    Tl, El, Kl, Hl, Fl = ws.Tl, ws.El, ws.Kl, ws.Hl, ws.Fl
     M = B * Tl
     lat, lon = m.local_grid
+    od = m.op_dtype
     ws.stats.zero_()
     gather_panels(m, g)
     K.patchify(ws.xin, ws.xp, B, lat, lon, m.local_vars, cfg.patch[0], cfg.patch[1])
@@ -250,11 +264,14 @@ def forward_grid(m, ws) -> None:
     for j in range(nj):
         b = f"block{j % cfg.n_blocks}."
         ctx.all_reduce_row(ws.st1[j])
-        K.ln_apply(ws.res[j], ws.st1[j], p[b + "ln1.gamma"].data, p[b + "ln1.beta"].data, ws.u[j], ws.mr1[j],
-                   M, El, E, m.eps)
+        hu = g.row.dest((M, El), od, slot=f"u_row{j}")          # LN1 output pushed to the row group
+        K.ln_apply(ws.res[j], ws.st1[j], p[b + "ln1.gamma"].data, p[b + "ln1.beta"].data, hu.own, ws.mr1[j],
+                   M, El, E, m.eps, bcast=hu.peers)
+        g.row.publish(hu)
+        uall = hu.planes.view(C, B, Tl, El)
         for bi in range(B):
-            tok1_fwd(m, g, ws, j, bi, b)
-            tok2_fwd(m, g, ws, j, bi, b)
+            acol = tok1_fwd(m, g, ws, j, bi, b, uall[:, bi])
+            tok2_fwd(m, g, ws, j, bi, b, acol)
         ctx.all_reduce_row(ws.st2[j])
         K.ln_apply(ws.x2[j], ws.st2[j], p[b + "ln2.gamma"].data, p[b + "ln2.beta"].data, ws.v[j], ws.mr2[j],
                    M, El, E, m.eps)
@@ -276,28 +293,43 @@ def backward_grid(m, ws) -> None:
     E, H, F = cfg.d_emb, cfg.d_ch, cfg.patch_features
     Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
     M = B * Tl
+    od = m.op_dtype
     ws.bstats.zero_()
-    gf, gop = ws.g, ws.g_op
-    cp = gop is not gf
+    gf = ws.g
+    # decoder: g = gd Wdec, its operand copy pushed to the row group for ch2's backward
+    hg = g.row.dest((M, El), od)
     chan_bwd(m, g, ws.gd, ws.y_op, _panel(m, g, "dec.w"), M, El, F, "dec.w", "dec.b", ws.gd, dX=gf,
-             epi=E_CP if cp else 0, d2=gop if cp else None)
+             epi=E_CP, d2=hg.own, d2_bcast=hg.peers)
+    g.row.publish(hg)
     nj = ws.r * cfg.n_blocks
     for j in reversed(range(nj)):
         b = f"block{j % cfg.n_blocks}."
-        chan_bwd(m, g, gop, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b", gf,
-                 dX=ws.gc, epi=E_GB, pre=ws.c[j])
-        chan_bwd(m, g, ws.gc, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, b + "ch1.w", b + "ch1.b", ws.gc,
-                 dX=ws.gv)
-        m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, ws.gx2_op, M, El, E,
-                  row_reduce=ctx.all_reduce_row)
+        # ch2: gc = (g Wc2) * gelu'(c), pushed to the row group for ch1's backward
+        hc = g.row.dest((M, Hl), od)
+        chan_bwd(m, g, None, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b", gf,
+                 dX=hc.own, dyrow=hg.planes, epi=E_GB, pre=ws.c[j], d_bcast=hc.peers)
+        g.row.publish(hc)
+        chan_bwd(m, g, None, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, b + "ch1.w", b + "ch1.b", hc.own,
+                 dX=ws.gv, dyrow=hc.planes)
+        hx = g.row.dest((M, El), od)                            # g_x2 operand copy -> row group
+        m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, hx.own, M, El, E,
+                  row_reduce=ctx.all_reduce_row, bcast=hx.peers)
+        g.row.publish(hx)
+        xall = hx.planes.view(m.C, B, Tl, El)
+        acol_all = g.col.persistent(f"a_col{j}").view(B, -1, Kl) if m.R > 1 else None
+        ghcols = []
         for bi in range(B):
-            tok2_bwd(m, g, ws, j, bi, b)
-        K.colsum(ws.gh, p[b + "tok1.b"].grad, B * Er, Kl)
+            acol = acol_all[bi] if m.R > 1 else ws.a[j][bi]
+            gh_local, ghcol = tok2_bwd(m, g, ws, j, bi, b, xall[:, bi], acol)
+            K.colsum(gh_local, p[b + "tok1.b"].grad, Er, Kl)
+            ghcols.append(ghcol)
         for bi in range(B):
-            tok1_bwd(m, g, ws, j, bi, b)
-        m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, gop, M, El, E,
-                  row_reduce=ctx.all_reduce_row)
-    chan_bwd(m, g, gop, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, "enc.w", "enc.b", gf)
+            tok1_bwd(m, g, ws, j, bi, b, ghcols[bi])
+        hg = g.row.dest((M, El), od)                            # g operand copy -> row group
+        m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, hg.own, M, El, E,
+                  row_reduce=ctx.all_reduce_row, bcast=hg.peers)
+        g.row.publish(hg)
+    chan_bwd(m, g, None, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, "enc.w", "enc.b", gf, dyrow=hg.planes)
 
 
 def grad_sync(m) -> None:

@@ -20,9 +20,14 @@ def gemm(out, a, b, am, bm, m, n, k, *batch_args, **kw):
     return T.gemm_into(out, a, b, am, bm, m, n, k, *batch_args, **kw)
 
 
+def _bref(addrs):
+    b = _lib.make_bcast(addrs)
+    return None if b is None else ctypes.byref(b)
+
+
 def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0,
              d2=None, ldd2=None, d2_bs=0, bias=None, bias_bs=0, resid=None, ldr=None, r_bs=0, pre=None, ldp=None,
-             p_bs=0, stats=None, stats_bs=0):
+             p_bs=0, stats=None, stats_bs=0, d_bcast=None, d2_bcast=None):
     """jg_epilogue: the GEMM epilogue applied to an accumulator `acc` [batch][m][acc_ld], or to the
     sum of `nplanes` partial planes of `acc` (plane stride acc_bs)."""
     g = _lib.GemmDesc()
@@ -39,6 +44,10 @@ def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alp
         g.pre, g.ldp, g.p_bstride, g.pre_type = pre.data_ptr(), ldp if ldp is not None else n, p_bs, _lib.dtype_code(pre)
     if stats is not None:
         g.stats, g.stats_bstride = stats.data_ptr(), stats_bs
+    for fld, addrs in (("d_bcast", d_bcast), ("d2_bcast", d2_bcast)):
+        bc = _lib.make_bcast(addrs)
+        if bc is not None:
+            setattr(g, fld, bc)
     _lib.call("jg_epilogue", ctypes.byref(g), acc.data_ptr(), _lib.dtype_code(acc), acc_ld if acc_ld is not None else n,
               acc_bs, nplanes)
 
@@ -69,9 +78,9 @@ def ln_moments(x, stats, rows, cols):
     _lib.call("jg_ln_moments", x.data_ptr(), stats.data_ptr(), rows, cols, cols)
 
 
-def ln_apply(x, stats, gamma, beta, y, mean_rstd, rows, cols, c_total, eps):
+def ln_apply(x, stats, gamma, beta, y, mean_rstd, rows, cols, c_total, eps, bcast=None):
     _lib.call("jg_ln_apply", x.data_ptr(), stats.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
-              _lib.dtype_code(y), ptr(mean_rstd), rows, cols, c_total, float(eps))
+              _lib.dtype_code(y), ptr(mean_rstd), rows, cols, c_total, float(eps), _bref(bcast))
 
 
 def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
@@ -79,10 +88,11 @@ def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
               bstats.data_ptr(), rows, cols)
 
 
-def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total):
+def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total,
+                 bcast=None):
     _lib.call("jg_ln_bwd_apply", x.data_ptr(), g.data_ptr(), gamma.data_ptr(), mean_rstd.data_ptr(),
               bstats.data_ptr(), ptr(resid), out.data_ptr(), None if out_op is None or out_op is out else out_op.data_ptr(),
-              ptr(dgamma), ptr(dbeta), None, rows, cols, c_total)
+              ptr(dgamma), ptr(dbeta), None, rows, cols, c_total, _bref(bcast))
 
 
 def colsum(x, out, rows, cols, ld=None):
@@ -94,12 +104,12 @@ def rowsum(x, out, rows, cols, ld=None):
 
 
 def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blend, g_dec, batch, lat, lon, chans,
-               pl, pw, inv_count, loss_scale):
+               pl, pw, inv_count, loss_scale, bcast=None):
     f32 = g_dec if g_dec is not None and g_dec.dtype == torch.float32 else None
     b16 = g_dec if g_dec is not None and g_dec.dtype == torch.bfloat16 else None
     _lib.call("jg_blend_loss", dec.data_ptr(), xin.data_ptr(), ptr(target), blend_w.data_ptr(), lat_w.data_ptr(),
               var_w.data_ptr(), ptr(g_ext), ptr(out), ptr(loss), ptr(g_blend), ptr(f32), ptr(b16),
-              batch, lat, lon, chans, pl, pw, float(inv_count), float(loss_scale))
+              batch, lat, lon, chans, pl, pw, float(inv_count), float(loss_scale), _bref(bcast))
 
 
 def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None):

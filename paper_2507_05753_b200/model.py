@@ -474,7 +474,7 @@ class WeatherMixerModel:
         self._gemm(out, g_op, ws.xp, MN, MN, E, F, M, **kw)
         K.colsum(g, p["enc.b"].grad, M, E)
 
-    def _ln_bwd(self, x, gin, pre, mr, bst, resid, out, out_op, rows, cols, c_total=None, row_reduce=None):
+    def _ln_bwd(self, x, gin, pre, mr, bst, resid, out, out_op, rows, cols, c_total=None, row_reduce=None, bcast=None):
         """Two-phase layer-norm backward + residual add (model.py:242-250): row sums (all-reduced
         over the row group by `row_reduce` when the normalised axis is split), then apply."""
         p = self.params
@@ -483,7 +483,7 @@ class WeatherMixerModel:
         if row_reduce is not None:
             row_reduce(bst)
         K.ln_bwd_apply(x, gin, p[pre + "gamma"].data, mr, bst, resid, out, out_op, p[pre + "gamma"].grad,
-                       p[pre + "beta"].grad, rows, cols, c_total)
+                       p[pre + "beta"].grad, rows, cols, c_total, bcast=bcast)
 
     # grid paths are implemented in jigsaw_grid.py (bound below)
     def _forward_grid(self, ws):

@@ -82,7 +82,7 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
               stats_bs: int = 0, d_bs: int | None = None, d2_bs: int | None = None,
               lda: int | None = None, ldb: int | None = None, ldd: int | None = None,
               a_lo: torch.Tensor | None = None, b_lo: torch.Tensor | None = None, adam=None,
-              d_planes=None) -> torch.Tensor:
+              d_planes=None, d_bcast=None, d2_bcast=None) -> torch.Tensor:
     """Low-level fused GEMM: out[b] (op)= sum_k A[b](m,k) B[b](n,k) with epilogue `epi`.
 
     A/B majors follow include/jigsaw_sm100.h. fp32 operands run 3xTF32: the hi/lo split is
@@ -122,6 +122,10 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
     if d_planes is not None:
         for i, addr in enumerate(d_planes):
             d.d_planes[i] = addr
+    for fld, addrs in (("d_bcast", d_bcast), ("d2_bcast", d2_bcast)):
+        bc = _lib.make_bcast(addrs)
+        if bc is not None:
+            setattr(d, fld, bc)
     if adam is not None:
         # adam = (m_view, v_view, bf16_copy_view | None, step_counter, lr, beta1, beta2, eps); out = master
         am, av, apb, astep, lr, b1, b2, eps = adam
@@ -272,7 +276,7 @@ def layer_norm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: fl
     stats = ln_stats(x)
     y = torch.empty_like(x)
     _lib.call("jg_ln_apply", x.data_ptr(), stats.data_ptr(), gamma.contiguous().data_ptr(),
-              beta.contiguous().data_ptr(), y.data_ptr(), _lib.JG_F32, None, rows, c, c, float(eps))
+              beta.contiguous().data_ptr(), y.data_ptr(), _lib.JG_F32, None, rows, c, c, float(eps), None)
     return y
 
 
@@ -288,7 +292,7 @@ def layer_norm_backward(x: torch.Tensor, gamma: torch.Tensor, eps: float, upstre
     scratch = torch.empty_like(x)
     zeros = torch.zeros_like(gamma)
     _lib.call("jg_ln_apply", x.data_ptr(), stats.data_ptr(), gamma.data_ptr(), zeros.data_ptr(),
-              scratch.data_ptr(), _lib.JG_F32, mr.data_ptr(), rows, c, c, float(eps))
+              scratch.data_ptr(), _lib.JG_F32, mr.data_ptr(), rows, c, c, float(eps), None)
     bstats = torch.zeros((rows, 2), dtype=torch.float32, device=x.device)
     _lib.call("jg_ln_bwd_moments", x.data_ptr(), upstream.data_ptr(), gamma.data_ptr(), mr.data_ptr(),
               bstats.data_ptr(), rows, c)
@@ -297,7 +301,7 @@ def layer_norm_backward(x: torch.Tensor, gamma: torch.Tensor, eps: float, upstre
     dbeta = torch.zeros_like(gamma)
     _lib.call("jg_ln_bwd_apply", x.data_ptr(), upstream.data_ptr(), gamma.data_ptr(), mr.data_ptr(),
               bstats.data_ptr(), None, dx.data_ptr(), None, dgamma.data_ptr(), dbeta.data_ptr(), None,
-              rows, c, c)
+              rows, c, c, None)
     return dx, dgamma, dbeta
 
 

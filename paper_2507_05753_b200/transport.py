@@ -27,6 +27,15 @@ import torch.distributed as dist
 from . import kernels as K
 
 
+class Gather:
+    """A reserved all-gather destination: the producer writes its block to `own` and (symmetric
+    memory) also stores it at every address in `peers`; after publish(), `planes` [G, *shape]
+    holds every member's block."""
+
+    def __init__(self, planes, own, peers):
+        self.planes, self.own, self.peers = planes, own, peers
+
+
 class NcclTransport:
     kind = "nccl"
 
@@ -59,6 +68,23 @@ class NcclTransport:
         else:
             dist.all_gather_into_tensor(out.view(-1), x.reshape(-1), group=self.group)
         return out
+
+    def dest(self, shape, dtype, slot: str | None = None, sub: int = 0, nsub: int = 1) -> Gather:
+        n = 1
+        for s_ in shape:
+            n *= s_
+        if slot is not None:
+            planes = self._persist[slot].view(nsub, self.G, *shape)[sub]
+        else:  # two rotating scratch buffers, like the symmetric-memory regions
+            self._k = getattr(self, "_k", 0) + 1
+            planes = self._buf(("ag", self._k % 2), self.G * n, dtype).view(self.G, *shape)
+        return Gather(planes, self._buf(("own", tuple(shape)), n, dtype).view(*shape), [])
+
+    def publish(self, h: Gather) -> None:
+        if self.G == 1:
+            h.planes[0].copy_(h.own)
+        else:
+            dist.all_gather_into_tensor(h.planes.view(-1), h.own.reshape(-1), group=self.group)
 
     def rs_gemm(self, rows: int, cols: int, dtype, fn, q: int = 1, out: torch.Tensor | None = None):
         """fn(s, D, d_bs, d_planes) for s < q computes GEMM batches j writing owner plane j*q + s."""
@@ -133,6 +159,23 @@ class SymmTransport:
             K.copy_async(self.base[j] + off + self.idx * nbytes, x, nbytes)
         self.barrier()
         return self._view(off, (self.G, *x.shape), x.dtype)
+
+    def dest(self, shape, dtype, slot: str | None = None, sub: int = 0, nsub: int = 1) -> Gather:
+        n = 1
+        for s_ in shape:
+            n *= s_
+        nbytes = n * torch.empty((), dtype=dtype).element_size()
+        if slot is not None:
+            off = self.offsets[slot][0] + sub * self.G * nbytes
+        else:
+            off = self._region()
+            assert self.G * nbytes <= self.scratch_bytes
+        planes = self._view(off, (self.G, *shape), dtype)
+        peers = [self.base[j] + off + self.idx * nbytes for j in range(self.G) if j != self.idx]
+        return Gather(planes, planes[self.idx], peers)
+
+    def publish(self, h: Gather) -> None:
+        self.barrier()
 
     def rs_gemm(self, rows: int, cols: int, dtype, fn, q: int = 1, out: torch.Tensor | None = None):
         es = torch.empty((), dtype=dtype).element_size()

@@ -55,8 +55,9 @@ def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias
 
 def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=False, epi=0, alpha=1.0, d2=None,
          bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
-         d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None, d_planes=None):
-    assert d_planes is None, "the CPU double has no peer memory"
+         d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None, d_planes=None, d_bcast=None,
+         d2_bcast=None):
+    assert d_planes is None and not d_bcast and not d2_bcast, "the CPU double has no peer memory"
     lda = lda if lda is not None else (k if am == KM else m)
     ldb = ldb if ldb is not None else (k if bm == KM else n)
     ldd = ldd if ldd is not None else n
@@ -98,7 +99,8 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
 
 def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0,
              d2=None, ldd2=None, d2_bs=0, bias=None, bias_bs=0, resid=None, ldr=None, r_bs=0, pre=None, ldp=None,
-             p_bs=0, stats=None, stats_bs=0):
+             p_bs=0, stats=None, stats_bs=0, d_bcast=None, d2_bcast=None):
+    assert not d_bcast and not d2_bcast
     acc_ld = acc_ld if acc_ld is not None else n
     for ob in range(batch):
         if nplanes > 1:
@@ -141,7 +143,8 @@ def ln_moments(x, stats, rows, cols):
     stats.view(rows, 2)[:, 1] += (xv * xv).sum(1).float()
 
 
-def ln_apply(x, stats, gamma, beta, y, mean_rstd, rows, cols, c_total, eps):
+def ln_apply(x, stats, gamma, beta, y, mean_rstd, rows, cols, c_total, eps, bcast=None):
+    assert not bcast
     st = stats.reshape(rows, 2).double()
     mean = st[:, 0] / c_total
     var = st[:, 1] / c_total - mean * mean
@@ -161,7 +164,9 @@ def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
     bs[:, 1] += (h * xh).sum(1).float()
 
 
-def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total):
+def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total,
+                 bcast=None):
+    assert not bcast
     mr = mean_rstd.reshape(rows, 2).double()
     xh = (x.reshape(rows, cols).double() - mr[:, :1]) * mr[:, 1:]
     gv = g.reshape(rows, cols).double()
@@ -188,7 +193,8 @@ def rowsum(x, out, rows, cols, ld=None):
 
 
 def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blend, g_dec, batch, lat, lon, chans,
-               pl, pw, inv_count, loss_scale):
+               pl, pw, inv_count, loss_scale, bcast=None):
+    assert not bcast
     decoded = _unpatchify(dec.double(), batch, lat, lon, chans, pl, pw)
     x = xin.double()
     w = blend_w.double()

@@ -59,7 +59,7 @@ def test_shape_errors_raise_before_launch(lib):
     with pytest.raises(ShapeError, match="empty problem"):
         _lib._check(_lib.load().jg_gemm(ctypes.byref(d), None), "jg_gemm")
     with pytest.raises(ShapeError, match="eps"):
-        _lib._check(_lib.load().jg_ln_apply(None, None, None, None, None, 0, None, 4, 4, 4, ctypes.c_float(0.0), None),
+        _lib._check(_lib.load().jg_ln_apply(None, None, None, None, None, 0, None, 4, 4, 4, ctypes.c_float(0.0), None, None),
                     "jg_ln_apply")
     with pytest.raises(ShapeError, match="not divisible"):
         _lib._check(_lib.load().jg_patchify(None, None, 0, 1, 5, 8, 2, 2, 2, None), "jg_patchify")
