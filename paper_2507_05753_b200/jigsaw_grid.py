@@ -68,18 +68,20 @@ class GridWorkspace:
         self.q = max(1, R // C)  # column-group owner chunks per row-gathered plane
         panel_shape = {"enc.w": (E, Fl), "ch1.w": (H, El), "ch2.w": (E, Hl), "dec.w": (F, El)}
         self.panel_names = [n for n in m.params if _base(n) in CHANNEL_LAYERS] if R > 1 else []
+        nmax = max(E, H, F)
         row_persist = [(f"u_row{j}", (C, B, Tl, El), od) for j in range(nj)]  # plane-major: LN writes its plane
-        col_persist = []
+        row_persist += [("g", (C, M, El), od), ("gc", (C, M, Hl), od), ("gx2", (C, M, El), od),
+                        ("tmp", (C, M, nmax // C), od)]
+        col_persist = [("tmp", (R, max(E * Kl, max(E * Fl, H * El, E * Hl, F * El) // R)), od)]
         if R > 1:
             col_persist += [(f"a_col{j}", (B, R, Er, Kl), od) for j in range(nj)]
             col_persist += [("gh_col", (B, R, Er, Kl), od)]
             col_persist += [(f"panel:{n}", (R, panel_shape[_base(n)][0] // R, panel_shape[_base(n)][1]), od)
                             for n in self.panel_names]
-        es, ps = torch.empty((), dtype=od).element_size(), 4
-        nmax = max(E, H, F)
-        row_scratch = max(M * nmax * ps, M * nmax * es, Tl * E * ps, Tl * E * es)
+        ps = 4
+        row_scratch = max(M * nmax * ps, Tl * E * ps)
         kin_max = max(E * Fl, H * El, E * Hl, F * El)
-        col_scratch = max(E * Kl * ps, kin_max * ps, E * Kl * es)
+        col_scratch = max(E * Kl * ps, kin_max * ps)
         kind = os.environ.get("JIGSAW_TRANSPORT", "symm" if dev.type == "cuda" else "nccl")
         if kind == "symm":
             self.row = SymmTransport(ctx.row_group, C, m.c, dev, row_scratch, row_persist) if C > 1 else None
@@ -87,10 +89,10 @@ class GridWorkspace:
         else:
             self.row = NcclTransport(ctx.row_group, C, m.c, dev) if C > 1 else None
             self.col = NcclTransport(ctx.col_group, R, m.r, dev) if R > 1 else None
-            for name, shape, dt in row_persist:
-                self.row.reserve(name, shape, dt)
-            for name, shape, dt in col_persist:
-                self.col.reserve(name, shape, dt)
+            for tr, spec in ((self.row, row_persist), (self.col, col_persist)):
+                if tr is not None:
+                    for name, shape, dt in spec:
+                        tr.reserve(name, shape, dt)
         self.kind = kind
         self.dgrad = torch.empty(max(kin_max, E * Kl), dtype=F32, device=dev)  # reduced weight gradients
         self.panels = {n: self.col.persistent(f"panel:{n}").view(panel_shape[_base(n)]) for n in self.panel_names}
@@ -297,7 +299,7 @@ def backward_grid(m, ws) -> None:
     ws.bstats.zero_()
     gf = ws.g
     # decoder: g = gd Wdec, its operand copy pushed to the row group for ch2's backward
-    hg = g.row.dest((M, El), od)
+    hg = g.row.dest((M, El), od, slot="g")
     chan_bwd(m, g, ws.gd, ws.y_op, _panel(m, g, "dec.w"), M, El, F, "dec.w", "dec.b", ws.gd, dX=gf,
              epi=E_CP, d2=hg.own, d2_bcast=hg.peers)
     g.row.publish(hg)
@@ -305,13 +307,13 @@ def backward_grid(m, ws) -> None:
     for j in reversed(range(nj)):
         b = f"block{j % cfg.n_blocks}."
         # ch2: gc = (g Wc2) * gelu'(c), pushed to the row group for ch1's backward
-        hc = g.row.dest((M, Hl), od)
+        hc = g.row.dest((M, Hl), od, slot="gc")
         chan_bwd(m, g, None, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b", gf,
                  dX=hc.own, dyrow=hg.planes, epi=E_GB, pre=ws.c[j], d_bcast=hc.peers)
         g.row.publish(hc)
         chan_bwd(m, g, None, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, b + "ch1.w", b + "ch1.b", hc.own,
                  dX=ws.gv, dyrow=hc.planes)
-        hx = g.row.dest((M, El), od)                            # g_x2 operand copy -> row group
+        hx = g.row.dest((M, El), od, slot="gx2")                # g_x2 operand copy -> row group
         m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, hx.own, M, El, E,
                   row_reduce=ctx.all_reduce_row, bcast=hx.peers)
         g.row.publish(hx)
@@ -325,7 +327,7 @@ def backward_grid(m, ws) -> None:
             ghcols.append(ghcol)
         for bi in range(B):
             tok1_bwd(m, g, ws, j, bi, b, ghcols[bi])
-        hg = g.row.dest((M, El), od)                            # g operand copy -> row group
+        hg = g.row.dest((M, El), od, slot="g")                  # g operand copy -> row group
         m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, hg.own, M, El, E,
                   row_reduce=ctx.all_reduce_row, bcast=hg.peers)
         g.row.publish(hg)

@@ -482,6 +482,14 @@ class WeatherMixerModel:
         K.ln_bwd_moments(x, gin, p[pre + "gamma"].data, mr, bst, rows, cols)
         if row_reduce is not None:
             row_reduce(bst)
+        if out_op is not None and out_op is not out and out_op.dtype == torch.float32:
+            # fp32 mode: the kernel's operand copy is bf16-only; copy (and push) the fp32 result
+            K.ln_bwd_apply(x, gin, p[pre + "gamma"].data, mr, bst, resid, out, None, p[pre + "gamma"].grad,
+                           p[pre + "beta"].grad, rows, cols, c_total)
+            out_op.view(-1).copy_(out.view(-1))
+            for addr in bcast or []:
+                K.copy_async(addr, out, out.numel() * 4)
+            return
         K.ln_bwd_apply(x, gin, p[pre + "gamma"].data, mr, bst, resid, out, out_op, p[pre + "gamma"].grad,
                        p[pre + "beta"].grad, rows, cols, c_total, bcast=bcast)
 

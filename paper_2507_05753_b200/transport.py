@@ -14,10 +14,12 @@ Two implementations of the same two operations used by jigsaw_grid.py:
   stores each partial plane straight into its owner's buffer (`d_planes`, remote st.global
   over NVLink, overlapping the transfer with the MMA tile by tile); gathers are copy-engine
   pushes into the peers' buffers; a 7 us device barrier (graph-capturable) publishes them.
-  Buffers: one symmetric arena per group = persistent slots (gathered tensors that live for the
-  whole step: u rows, gelu(h) columns, weight panels) + two rotating scratch regions, so an
-  exchange never overwrites a region a peer may still be reading (the barrier of exchange k+1
-  orders it after every rank's consumer of exchange k-1).
+  Buffers: one symmetric arena per group = a named slot per gather role (u rows, gelu(h)
+  columns, weight panels, the g / gc / g_x2 gradient gathers, a copy-engine scratch) + two
+  rotating regions for reduce-scatter partials. A slot is rewritten only after the barrier of a
+  later exchange, which every member passes only after its consumer of the previous contents
+  (stream order), so no peer can overwrite data another member is still reading; partial
+  planes are summed right after their barrier, so two rotating regions suffice.
 """
 from __future__ import annotations
 
@@ -50,6 +52,14 @@ class NcclTransport:
     def persistent(self, name: str) -> torch.Tensor:
         return self._persist[name]
 
+    def _slot(self, name, numel, dtype):
+        t = self._persist.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            assert name not in self._persist or t.numel() >= numel, f"slot {name} too small"
+            t = torch.empty(numel, dtype=dtype, device=self.device)
+            self._persist[name] = t
+        return t.reshape(-1)[:numel]
+
     def _buf(self, key, numel, dtype):
         b = self._scratch.get((key, dtype))
         if b is None or b.numel() < numel:
@@ -57,28 +67,21 @@ class NcclTransport:
             self._scratch[(key, dtype)] = b
         return b[:numel]
 
-    def ag(self, x: torch.Tensor, slot: str | None = None, sub: int = 0, nsub: int = 1) -> torch.Tensor:
-        """Planes [G, *x.shape]; `slot` = persistent destination (viewed [nsub, G, *x.shape], entry sub)."""
-        if slot is not None:
-            out = self._persist[slot].view(nsub, self.G, *x.shape)[sub]
-        else:
-            out = self._buf("ag", self.G * x.numel(), x.dtype).view(self.G, *x.shape)
+    def ag(self, x: torch.Tensor, slot: str = "tmp", sub: int = 0, nsub: int = 1) -> torch.Tensor:
+        """Planes [G, *x.shape] in the named slot (viewed [nsub, G, *x.shape], entry sub)."""
+        out = self._slot(slot, nsub * self.G * x.numel(), x.dtype).view(nsub, self.G, *x.shape)[sub]
         if self.G == 1:
             out[0].copy_(x)
         else:
             dist.all_gather_into_tensor(out.view(-1), x.reshape(-1), group=self.group)
         return out
 
-    def dest(self, shape, dtype, slot: str | None = None, sub: int = 0, nsub: int = 1) -> Gather:
+    def dest(self, shape, dtype, slot: str, sub: int = 0, nsub: int = 1) -> Gather:
         n = 1
         for s_ in shape:
             n *= s_
-        if slot is not None:
-            planes = self._persist[slot].view(nsub, self.G, *shape)[sub]
-        else:  # two rotating scratch buffers, like the symmetric-memory regions
-            self._k = getattr(self, "_k", 0) + 1
-            planes = self._buf(("ag", self._k % 2), self.G * n, dtype).view(self.G, *shape)
-        return Gather(planes, self._buf(("own", tuple(shape)), n, dtype).view(*shape), [])
+        planes = self._slot(slot, nsub * self.G * n, dtype).view(nsub, self.G, *shape)[sub]
+        return Gather(planes, self._buf(("own", slot), n, dtype).view(*shape), [])
 
     def publish(self, h: Gather) -> None:
         if self.G == 1:
@@ -147,29 +150,29 @@ class SymmTransport:
     def barrier(self) -> None:
         self.hdl.barrier(channel=0)
 
-    def ag(self, x: torch.Tensor, slot: str | None = None, sub: int = 0, nsub: int = 1) -> torch.Tensor:
+    def _slot_off(self, slot: str, sub: int, nbytes: int) -> int:
+        off, shape, dtype = self.offsets[slot]
+        cap = torch.empty((), dtype=dtype).element_size()
+        for s_ in shape:
+            cap *= s_
+        assert (sub + 1) * self.G * nbytes <= cap, f"slot {slot} too small"
+        return off + sub * self.G * nbytes
+
+    def ag(self, x: torch.Tensor, slot: str = "tmp", sub: int = 0, nsub: int = 1) -> torch.Tensor:
         nbytes = x.numel() * x.element_size()
-        if slot is not None:
-            off = self.offsets[slot][0] + sub * self.G * nbytes
-        else:
-            off = self._region()
-            assert self.G * nbytes <= self.scratch_bytes
+        off = self._slot_off(slot, sub, nbytes)
         x = x.contiguous()
         for j in range(self.G):  # push my block into slot idx of every member (copy engine)
             K.copy_async(self.base[j] + off + self.idx * nbytes, x, nbytes)
         self.barrier()
         return self._view(off, (self.G, *x.shape), x.dtype)
 
-    def dest(self, shape, dtype, slot: str | None = None, sub: int = 0, nsub: int = 1) -> Gather:
+    def dest(self, shape, dtype, slot: str, sub: int = 0, nsub: int = 1) -> Gather:
         n = 1
         for s_ in shape:
             n *= s_
         nbytes = n * torch.empty((), dtype=dtype).element_size()
-        if slot is not None:
-            off = self.offsets[slot][0] + sub * self.G * nbytes
-        else:
-            off = self._region()
-            assert self.G * nbytes <= self.scratch_bytes
+        off = self._slot_off(slot, sub, nbytes)
         planes = self._view(off, (self.G, *shape), dtype)
         peers = [self.base[j] + off + self.idx * nbytes for j in range(self.G) if j != self.idx]
         return Gather(planes, planes[self.idx], peers)

@@ -19,7 +19,8 @@ for axis in ("row", "col"):
         continue
     grp = ctx.row_group if axis == "row" else ctx.col_group
     idx = ctx.c if axis == "row" else ctx.r
-    st = SymmTransport(grp, G, idx, dev, 64 << 20, [("keep", (3, G, 128, 64), torch.bfloat16)])
+    st = SymmTransport(grp, G, idx, dev, 64 << 20, [("keep", (3, G, 128, 64), torch.bfloat16),
+                                                    ("tmp", (G, 128, 64), torch.bfloat16)])
     nt = NcclTransport(grp, G, idx, dev)
     x = torch.randn(128, 64, device=dev).bfloat16()
     a = st.ag(x)
