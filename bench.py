@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--no-fused-adam", action="store_true", help="separate Adam kernel instead of the GEMM epilogue")
+    ap.add_argument("--fused-adam", action="store_true", help="Adam inside the weight-gradient GEMM epilogue")
     return ap.parse_args()
 
 
@@ -177,7 +177,7 @@ def run_ours(args, rank, world):
     big = cfg.train_flops() > 1e12
     model = WeatherMixerModel(ctx, cfg, seed=0, dtype=args.dtype, init="fast" if big else "reference")
     model.lat_real, model.vars_real = lat_real, vars_real
-    step = TrainStep(model, batch=args.batch, graph=not args.no_graph, fused_adam=not args.no_fused_adam)
+    step = TrainStep(model, batch=args.batch, graph=not args.no_graph, fused_adam=args.fused_adam)
     # synthetic z-scored inputs: x, target ~ N(0, 1); padded rows / channels are zero
     lat, lon = model.local_grid
     nv = model.local_vars

@@ -362,63 +362,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           }
         }
         }  // row_ok: math done
-        if ((epi & JG_EPI_ADAM) && row_ok) {
-          // v[] is the complete gradient of this weight tile: update D (= master) in place.
-          // All 3 x 8 sixteen-byte loads of the chunk are issued before any math so each thread
-          // keeps ~384 B in flight (the epilogue is HBM-bound: 26 B per parameter).
+        if (epi & JG_EPI_ADAM) {
+          // v[] is the complete gradient of this weight tile. Transpose the warp's 32 x 32 chunk
+          // through its staging buffer (XOR swizzle) and update 4 rows x 32 columns per warp
+          // instruction: lane = (row-in-4, float4 column), every master / m / v access a full
+          // 128B row segment, all 24 vector loads of the chunk in flight before any math
+          // (the epilogue is HBM-bound: 26 B per parameter).
+          float* sf = reinterpret_cast<float*>(stg);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sf[lane * 32 + (j ^ lane)] = v[j];
+          __syncwarp();
           float* dp = reinterpret_cast<float*>(p.d);
-          if (full_chunk) {
-            float4 w4[8], m4[8], v4[8];
-            const float4* wsrc = reinterpret_cast<const float4*>(dp + drow + col0);
-            const float4* msrc = reinterpret_cast<const float4*>(p.adam_m + drow + col0);
-            const float4* vsrc = reinterpret_cast<const float4*>(p.adam_v + drow + col0);
+          const int sr = lane >> 3, c4 = (lane & 7) * 4;
+          const int col = col0 + c4;
+          const int rbase = m0 + q * 32;
+          float4 w4[8], m4[8], v4[8];
+          int64_t off[8];
+          bool ok[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              w4[i] = wsrc[i];
-              m4[i] = msrc[i];
-              v4[i] = vsrc[i];
+          for (int i = 0; i < 8; ++i) {
+            const int rr = rbase + i * 4 + sr;
+            off[i] = tb * p.d_bs + static_cast<int64_t>(rr) * p.ldd + col;
+            ok[i] = rr < p.m && col + 3 < p.n;
+            if (ok[i]) {
+              w4[i] = *reinterpret_cast<const float4*>(dp + off[i]);
+              m4[i] = *reinterpret_cast<const float4*>(p.adam_m + off[i]);
+              v4[i] = *reinterpret_cast<const float4*>(p.adam_v + off[i]);
             }
+          }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + sr;
+            if (ok[i]) {
               float* w = &w4[i].x;
               float* mm = &m4[i].x;
               float* vv = &v4[i].x;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float gj = v[i * 4 + j];
-                mm[j] = ab1 * mm[j] + (1.0f - ab1) * gj;
-                vv[j] = ab2 * vv[j] + (1.0f - ab2) * gj * gj;
-                w[j] -= alr * (mm[j] * bc1) / (sqrtf(vv[j] * bc2) + aeps);
+              for (int k = 0; k < 4; ++k) {
+                const float gj = sf[r * 32 + ((c4 + k) ^ r)];
+                mm[k] = ab1 * mm[k] + (1.0f - ab1) * gj;
+                vv[k] = ab2 * vv[k] + (1.0f - ab2) * gj * gj;
+                w[k] -= alr * (mm[k] * bc1) / (sqrtf(vv[k] * bc2) + aeps);
               }
-            }
-            float4* wdst = reinterpret_cast<float4*>(dp + drow + col0);
-            float4* mdst = reinterpret_cast<float4*>(p.adam_m + drow + col0);
-            float4* vdst = reinterpret_cast<float4*>(p.adam_v + drow + col0);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              wdst[i] = w4[i];
-              mdst[i] = m4[i];
-              vdst[i] = v4[i];
-            }
-            if (p.adam_pbf16) {
-              uint4* bdst = reinterpret_cast<uint4*>(p.adam_pbf16 + drow + col0);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                uint4 raw;
-                __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
-                h[0] = __floats2bfloat162_rn(w4[2 * i].x, w4[2 * i].y);
-                h[1] = __floats2bfloat162_rn(w4[2 * i].z, w4[2 * i].w);
-                h[2] = __floats2bfloat162_rn(w4[2 * i + 1].x, w4[2 * i + 1].y);
-                h[3] = __floats2bfloat162_rn(w4[2 * i + 1].z, w4[2 * i + 1].w);
-                bdst[i] = raw;
+              *reinterpret_cast<float4*>(dp + off[i]) = w4[i];
+              *reinterpret_cast<float4*>(p.adam_m + off[i]) = m4[i];
+              *reinterpret_cast<float4*>(p.adam_v + off[i]) = v4[i];
+              if (p.adam_pbf16) {
+                __nv_bfloat162 lo = __floats2bfloat162_rn(w[0], w[1]), hi = __floats2bfloat162_rn(w[2], w[3]);
+                uint2 raw;
+                raw.x = *reinterpret_cast<uint32_t*>(&lo);
+                raw.y = *reinterpret_cast<uint32_t*>(&hi);
+                *reinterpret_cast<uint2*>(p.adam_pbf16 + off[i]) = raw;
               }
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < ncol) {
-                const int64_t o = drow + col0 + j;
-                const float gj = v[j];
+            } else if (rbase + r < p.m) {  // ragged column tail: scalar
+              for (int k = 0; k < 4; ++k) {
+                if (col + k >= p.n) break;
+                const int64_t o = off[i] + k;
+                const float gj = sf[r * 32 + ((c4 + k) ^ r)];
                 const float mm = ab1 * p.adam_m[o] + (1.0f - ab1) * gj;
                 const float vv = ab2 * p.adam_v[o] + (1.0f - ab2) * gj * gj;
                 const float w = dp[o] - alr * (mm * bc1) / (sqrtf(vv * bc2) + aeps);

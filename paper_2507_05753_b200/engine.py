@@ -22,10 +22,14 @@ from .train import AdamConfig
 
 class TrainStep:
     def __init__(self, model: WeatherMixerModel, batch: int = 1, r: int = 1, adam: AdamConfig | None = None,
-                 graph: bool = True, loss_scale: float = 1.0, fused_adam: bool = True):
+                 graph: bool = True, loss_scale: float = 1.0, fused_adam: bool = False):
         self.model, self.batch, self.r = model, batch, r
-        # Adam fused into the weight-gradient GEMM epilogues: valid when every weight receives
-        # exactly one gradient GEMM per step (rollout 1; one sample per GEMM on the grid path).
+        # Every weight receives exactly one gradient GEMM per step at rollout 1 (one per sample
+        # on the grid path): the GEMM overwrites the fp32 gradient (no zeroing, no read-back) and
+        # one HBM-roofline Adam kernel per lr class follows. fused_adam=True instead applies Adam
+        # inside the weight-gradient GEMM epilogue (JG_EPI_ADAM; measured no faster on C4, the
+        # 4 epilogue warps cannot hide 26 B/param behind the MMA).
+        self.overwrite = r == 1
         self.fused_adam = fused_adam and r == 1 and (model.ctx.n == 1 or batch == 1)
         self.adam = adam or AdamConfig()
         self.loss_scale = loss_scale
@@ -44,8 +48,8 @@ class TrainStep:
     def _body(self) -> None:
         m, ws, f = self.model, self.ws, self.model.flat
         K.step_increment(self.step_count)
-        if self.fused_adam:
-            for cls in f.CLASSES:  # matrix gradients never hit HBM; only vector grads accumulate
+        if self.fused_adam or self.overwrite:
+            for cls in f.CLASSES:  # matrix gradients are written whole by their GEMM; vectors accumulate
                 lo, hi = f.vec_range(cls)
                 f.grad[lo:hi].zero_()
         else:
@@ -56,10 +60,12 @@ class TrainStep:
         if m.ctx.n > 1:
             m.ctx.all_reduce_all(ws.loss)  # the loss is a sum of per-tile terms
         m._fused_adam = (self.step_count, self.adam) if self.fused_adam else None
+        m._grad_overwrite = self.overwrite
         try:
             m._backward(ws)
         finally:
             m._fused_adam = None
+            m._grad_overwrite = False
         m.grad_sync()
         self._adam()
 

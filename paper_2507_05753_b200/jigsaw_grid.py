@@ -119,6 +119,9 @@ def _wgrad_planes(m, g, wname, acc, nplanes, plane_stride, numel):
     if nplanes == 1:
         m._wgrad_reduced(wname, acc)
         return
+    if getattr(m, "_grad_overwrite", False) and getattr(m, "_fused_adam", None) is None:
+        K.sum_planes(m.params[wname].grad, acc, numel, nplanes, plane_stride)  # straight into the gradient
+        return
     red = g.dgrad[:numel]
     K.sum_planes(red, acc, numel, nplanes, plane_stride)
     m._wgrad_reduced(wname, red.view(m.params[wname].data.shape))
@@ -225,7 +228,9 @@ def tok2_bwd(m, g, ws, j, bi, b, grow, acol):
         g.col.publish(hg)
         gh_local, ghcol = hg.own, hg.planes.view(-1, Kl)
     K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
-    out, kw = m._wgrad(b + "tok2.w") if B == 1 else (p[b + "tok2.w"].grad, {"epi": E_ACC})
+    out, kw = m._wgrad(b + "tok2.w") if bi == 0 or B == 1 else (p[b + "tok2.w"].grad, {"epi": E_ACC})
+    if bi == 0 and B > 1 and kw.get("epi") == _lib.EPI_ADAM:
+        out, kw = p[b + "tok2.w"].grad, {"epi": E_ACC}
     K.gemm(out, grow, acol, KM, MN, Tl, Kl, El, C, ps, El * Kl, reduce_batch=True, **kw)
     return gh_local, ghcol
 
@@ -242,7 +247,9 @@ def tok1_bwd(m, g, ws, j, bi, b, ghcol):
     if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
         K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
     urow = g.row.persistent(f"u_row{j}").view(C, B, Tl, El)[:, bi]
-    out, kw = m._wgrad(b + "tok1.w") if B == 1 else (p[b + "tok1.w"].grad, {"epi": E_ACC})
+    out, kw = m._wgrad(b + "tok1.w") if bi == 0 or B == 1 else (p[b + "tok1.w"].grad, {"epi": E_ACC})
+    if bi == 0 and B > 1 and kw.get("epi") == _lib.EPI_ADAM:
+        out, kw = p[b + "tok1.w"].grad, {"epi": E_ACC}
     K.gemm(out, urow, ghcol, KM, MN, Tl, Kl, El, C, B * Tl * El, El * Kl, reduce_batch=True, **kw)
 
 

@@ -408,7 +408,9 @@ class WeatherMixerModel:
         p = self.params[name]
         fa = getattr(self, "_fused_adam", None)
         if fa is None:
-            return p.grad, {"epi": E_ACC}
+            # inside TrainStep (rollout 1) each weight's gradient comes from exactly one GEMM:
+            # overwrite (TMA-store epilogue) instead of read-modify-write, no zeroing needed
+            return p.grad, {"epi": 0 if getattr(self, "_grad_overwrite", False) else E_ACC}
         step, cfg = fa
         f = self.flat
         return p.data, {"epi": _lib.EPI_ADAM, "adam": (f.view(name, f.m), f.view(name, f.v),
@@ -420,7 +422,10 @@ class WeatherMixerModel:
         p = self.params[name]
         fa = getattr(self, "_fused_adam", None)
         if fa is None:
-            K.axpy(p.grad, red)
+            if getattr(self, "_grad_overwrite", False):
+                K.sum_planes(p.grad, red, p.grad.numel(), 1, 0)
+            else:
+                K.axpy(p.grad, red)
             return
         step, cfg = fa
         f = self.flat
