@@ -123,10 +123,10 @@ int jg_epilogue(const jg_gemm_desc* desc, const void* acc, int32_t acc_type, int
 /* y += alpha * x (fp32): accumulate a reduce-scattered weight gradient (parallel.py:490-493). */
 int jg_axpy(float* y, const float* x, float alpha, int64_t n, void* stream);
 
-/* y = sum of nplanes fp32 planes x[p*plane_stride + i] (+ y if accumulate): reduce pushed
- * Jigsaw partials that need no epilogue (weight gradients). */
-int jg_sum_planes(float* y, const float* x, int64_t n, int32_t nplanes, int64_t plane_stride, int32_t accumulate,
-                  void* stream);
+/* y = sum of nplanes planes x[p*plane_stride + i] (x_type JG_F32 or JG_BF16; fp32 sum, + y if
+ * accumulate): reduce pushed Jigsaw partials that need no epilogue (weight gradients, gu). */
+int jg_sum_planes(float* y, const void* x, int32_t x_type, int64_t n, int32_t nplanes, int64_t plane_stride,
+                  int32_t accumulate, void* stream);
 
 /* Asynchronous device copy (copy engine; either side may be a peer GPU's buffer over NVLink).
  * Used to push Jigsaw activation tiles into peers' symmetric gather buffers. */

@@ -114,7 +114,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_sqnorm": [vp, i64, vp, vp],
         "jg_epilogue": [ctypes.POINTER(GemmDesc), vp, i32, i64, i64, i32, vp],
         "jg_axpy": [vp, vp, f32, i64, vp],
-        "jg_sum_planes": [vp, vp, i64, i32, i64, i32, vp],
+        "jg_sum_planes": [vp, vp, i32, i64, i32, i64, i32, vp],
         "jg_copy_async": [vp, vp, i64, vp],
     }
     for name, args in sig.items():

@@ -621,11 +621,31 @@ __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
   if (a.dbc.n || a.d2bc.n) __threadfence_system();
 }
 
-__global__ void sum_planes_kernel(float* __restrict__ y, const float* __restrict__ x, int64_t n, int nplanes,
-                                  int64_t ps, bool accumulate) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+template <bool BF>
+__global__ void sum_planes_kernel(float* __restrict__ y, const void* __restrict__ x, int64_t n, int nplanes,
+                                  int64_t ps, bool accumulate, bool vec) {
+  // vec: 8 consecutive elements per thread (16-byte loads / two 16-byte stores)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; i < n; i += stride * 8) {
+      float s[8], t[8];
+      if (accumulate) jgd::load8(y, i, false, s);
+      else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] = 0.f;
+      }
+      for (int p = 0; p < nplanes; ++p) {
+        jgd::load8(x, p * ps + i, BF, t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] += t[e];
+      }
+      jgd::store8(y, i, false, s);
+    }
+    return;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     float s = accumulate ? y[i] : 0.f;
-    for (int p = 0; p < nplanes; ++p) s += x[p * ps + i];
+    for (int p = 0; p < nplanes; ++p) s += jgd::load1(x, p * ps + i, BF);
     y[i] = s;
   }
 }
@@ -865,10 +885,14 @@ int jg_epilogue(const jg_gemm_desc* g, const void* acc, int32_t acc_type, int64_
   return JG_OK;
 }
 
-int jg_sum_planes(float* y, const float* x, int64_t n, int32_t nplanes, int64_t plane_stride, int32_t accumulate,
-                  void* stream) {
+int jg_sum_planes(float* y, const void* x, int32_t x_type, int64_t n, int32_t nplanes, int64_t plane_stride,
+                  int32_t accumulate, void* stream) {
   if (n == 0) return JG_OK;
-  sum_planes_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(y, x, n, nplanes, plane_stride, accumulate != 0);
+  const bool bf = x_type == JG_BF16;
+  const bool vec = n % 8 == 0 && plane_stride % 8 == 0 && al16(y) && al16(x);
+  const int64_t work = vec ? n / 8 : n;
+  if (bf) sum_planes_kernel<true><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(y, x, n, nplanes, plane_stride, accumulate != 0, vec);
+  else sum_planes_kernel<false><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(y, x, n, nplanes, plane_stride, accumulate != 0, vec);
   JG_LAUNCH_CHECK("sum_planes");
   return JG_OK;
 }

@@ -46,6 +46,11 @@ class TrainStep:
 
     # -- the step body --------------------------------------------------------------------
     def _body(self) -> None:
+        self._body_fwd()
+        self._body_bwd()
+
+    def _body_fwd(self) -> None:
+        """Step counter, gradient zeroing, forward (needs only x)."""
         m, ws, f = self.model, self.ws, self.model.flat
         K.step_increment(self.step_count)
         if self.fused_adam or self.overwrite:
@@ -55,6 +60,10 @@ class TrainStep:
         else:
             m.zero_grads()
         m._forward(ws)
+
+    def _body_bwd(self) -> None:
+        """Loss against the target, backward, gradient sync, Adam."""
+        m, ws = self.model, self.ws
         ws.loss.zero_()
         m._blend(ws, target=self.target, loss=ws.loss, loss_scale=self.loss_scale)
         if m.ctx.n > 1:
@@ -81,7 +90,9 @@ class TrainStep:
                    hi - lo, a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count)
 
     def capture(self) -> None:
-        """Warm up on a side stream, then capture the step into a CUDA graph."""
+        """Warm up on a side stream, then capture the step into two CUDA graphs (forward | loss +
+        backward + Adam) sharing one memory pool, so the public call can overlap the target's
+        host->device copy with the forward."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -91,29 +102,53 @@ class TrainStep:
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         # the warm-up was a real training step (Adam state and step counter advanced)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._body()
-        self.graph = g
+        g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            self._body_fwd()
+        with torch.cuda.graph(g2, pool=g1.pool()):
+            self._body_bwd()
+        self.graph = (g1, g2)
         torch.cuda.synchronize()
 
-    def run_device(self) -> torch.Tensor:
-        """One step on resident inputs (self.ws.xin / self.target); returns the device loss."""
+    def run_device(self, target_ready: torch.cuda.Event | None = None) -> torch.Tensor:
+        """One step on resident inputs (self.ws.xin / self.target); returns the device loss.
+        `target_ready`: event the loss half of the step waits on (target still in flight)."""
         if self.use_graph:
             if self.graph is None:
                 self.capture()
-            self.graph.replay()
+            self.graph[0].replay()
+            if target_ready is not None:
+                torch.cuda.current_stream().wait_event(target_ready)
+            self.graph[1].replay()
         else:
             before = _lib.launch_count()
-            self._body()
+            self._body_fwd()
+            if target_ready is not None:
+                torch.cuda.current_stream().wait_event(target_ready)
+            self._body_bwd()
             self.launches_per_step = _lib.launch_count() - before
         return self.ws.loss
 
     def __call__(self, x: torch.Tensor, target: torch.Tensor) -> float:
-        """Public step: copy this step's inputs from (pinned) host memory, run, read the loss."""
-        self.ws.xin.copy_(x, non_blocking=True)
-        self.target.copy_(target, non_blocking=True)
-        loss = self.run_device()
+        """Public step: copy this step's inputs from (pinned) host memory, run, read the loss.
+        The target is copied on a side stream while the forward runs."""
+        cur = torch.cuda.current_stream() if self.model.device.type == "cuda" else None
+        ev = None
+        if cur is not None:
+            if getattr(self, "_copy_stream", None) is None:
+                self._copy_stream = torch.cuda.Stream()
+                self._target_ev = torch.cuda.Event()
+            cs = self._copy_stream
+            cs.wait_stream(cur)  # the previous step's loss half has finished reading the target
+            self.ws.xin.copy_(x, non_blocking=True)
+            with torch.cuda.stream(cs):
+                self.target.copy_(target, non_blocking=True)
+                self._target_ev.record(cs)
+            ev = self._target_ev
+        else:
+            self.ws.xin.copy_(x)
+            self.target.copy_(target)
+        loss = self.run_device(ev)
         self._pinned_loss.copy_(loss, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return float(self._pinned_loss.item())

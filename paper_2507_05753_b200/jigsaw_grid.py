@@ -94,6 +94,10 @@ class GridWorkspace:
                     for name, shape, dt in spec:
                         tr.reserve(name, shape, dt)
         self.kind = kind
+        # reduce-scatter partial planes travel in the operand dtype (bf16 mode: half the NVLink bytes
+        # and half the epilogue reads; summed in fp32); JIGSAW_PARTIALS=fp32 keeps fp32 partials
+        bf = od == torch.bfloat16 and os.environ.get("JIGSAW_PARTIALS", "bf16") != "fp32"
+        self.pdt = torch.bfloat16 if bf else F32
         self.dgrad = torch.empty(max(kin_max, E * Kl), dtype=F32, device=dev)  # reduced weight gradients
         self.panels = {n: self.col.persistent(f"panel:{n}").view(panel_shape[_base(n)]) for n in self.panel_names}
 
@@ -116,7 +120,7 @@ def gather_panels(m, g) -> None:
 
 def _wgrad_planes(m, g, wname, acc, nplanes, plane_stride, numel):
     """Weight gradient that arrived as reduce-scatter planes: sum them into the gradient sink."""
-    if nplanes == 1:
+    if nplanes == 1 and acc.dtype == F32:
         m._wgrad_reduced(wname, acc)
         return
     if getattr(m, "_grad_overwrite", False) and getattr(m, "_fused_adam", None) is None:
@@ -136,7 +140,7 @@ def chan_fwd(m, g, X, panel, M, kin_l, nout, **epi):
     def fn(s, D, d_bs, dpl):
         K.gemm(D, X, panel, KM, KM, M, nl, kin_l, C, 0, nl * kin_l, d_bs=d_bs, d_planes=dpl)
 
-    acc, npl, ps = g.row.rs_gemm(M, nl, F32, fn)
+    acc, npl, ps = g.row.rs_gemm(M, nl, g.pdt, fn)
     K.epilogue(acc, M, nl, acc_bs=ps, nplanes=npl, **epi)
 
 
@@ -160,7 +164,7 @@ def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None
             K.gemm(D, dyrow[..., s * nr:], X, MN, MN, nr, kin_l, M, C, M * nl, 0, d_bs=d_bs, d_planes=dpl,
                    lda=nl)
 
-        acc, npl, ps = g.col.rs_gemm(nr, kin_l, F32, fn, q=q)
+        acc, npl, ps = g.col.rs_gemm(nr, kin_l, g.pdt, fn, q=q)
         _wgrad_planes(m, g, wname, acc, npl, ps, nr * kin_l)
     K.colsum(bias_src, m.params[bname].grad, M, nl)
 
@@ -183,7 +187,7 @@ def tok1_fwd(m, g, ws, j, bi, b, urow):
         K.gemm(D, urow[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
                d_planes=dpl, lda=El)
 
-    acc, npl, pst = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
+    acc, npl, pst = g.col.rs_gemm(Er, Kl, g.pdt, fn, q=q)
     ha = g.col.dest((Er, Kl), m.op_dtype, slot=f"a_col{j}", sub=bi, nsub=B)   # gelu(h) pushed to peers
     K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data,
                d=ws.h[j][bi], d2=ha.own, d2_bcast=ha.peers)
@@ -199,7 +203,7 @@ def tok2_fwd(m, g, ws, j, bi, b, acol):
     def fn(s, D, d_bs, dpl):
         K.gemm(D, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
 
-    acc, npl, ps = g.row.rs_gemm(Tl, El, F32, fn)
+    acc, npl, ps = g.row.rs_gemm(Tl, El, g.pdt, fn)
     K.epilogue(acc, Tl, El, acc_bs=ps, nplanes=npl, epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data,
                resid=ws.res[j][bi], d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
 
@@ -222,7 +226,7 @@ def tok2_bwd(m, g, ws, j, bi, b, grow, acol):
             K.gemm(D, grow[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
                    d_planes=dpl, lda=El)
 
-        acc, npl, pst = g.col.rs_gemm(Er, Kl, F32, fn, q=q)
+        acc, npl, pst = g.col.rs_gemm(Er, Kl, g.pdt, fn, q=q)
         hg = g.col.dest((Er, Kl), m.op_dtype, slot="gh_col", sub=bi, nsub=B)
         K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_GB, pre=ws.h[j][bi], d=hg.own, d_bcast=hg.peers)
         g.col.publish(hg)
@@ -243,7 +247,7 @@ def tok1_bwd(m, g, ws, j, bi, b, ghcol):
     def fn(s, D, d_bs, dpl):
         K.gemm(D, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
 
-    acc, npl, ps = g.row.rs_gemm(Tl, El, F32, fn, out=ws.gu[bi])
+    acc, npl, ps = g.row.rs_gemm(Tl, El, g.pdt, fn, out=ws.gu[bi])
     if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
         K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
     urow = g.row.persistent(f"u_row{j}").view(C, B, Tl, El)[:, bi]

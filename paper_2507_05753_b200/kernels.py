@@ -53,8 +53,9 @@ def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alp
 
 
 def sum_planes(y, x, n, nplanes, plane_stride, accumulate=False):
-    """y[:n] (+)= sum_p x[p * plane_stride + i] (fp32)."""
-    _lib.call("jg_sum_planes", y.data_ptr(), x.data_ptr(), n, nplanes, plane_stride, int(accumulate))
+    """y[:n] (+)= sum_p x[p * plane_stride + i] (x fp32 or bf16, y fp32)."""
+    _lib.call("jg_sum_planes", y.data_ptr(), x.data_ptr(), _lib.dtype_code(x), n, nplanes, plane_stride,
+              int(accumulate))
 
 
 def copy_async(dst_ptr: int, src: torch.Tensor, nbytes: int | None = None):

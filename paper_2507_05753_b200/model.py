@@ -425,7 +425,7 @@ class WeatherMixerModel:
             if getattr(self, "_grad_overwrite", False):
                 K.sum_planes(p.grad, red, p.grad.numel(), 1, 0)
             else:
-                K.axpy(p.grad, red)
+                K.sum_planes(p.grad, red, p.grad.numel(), 1, 0, accumulate=True)
             return
         step, cfg = fa
         f = self.flat

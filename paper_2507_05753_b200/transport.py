@@ -96,7 +96,8 @@ class NcclTransport:
             fn(s, planes[s], q * rows * cols, None)
         if self.G == 1:
             return planes[0], 1, 0
-        red = out if out is not None else self._buf("red", rows * cols, dtype).view(rows, cols)
+        use_out = out is not None and out.dtype == dtype
+        red = out if use_out else self._buf("red", rows * cols, dtype).view(rows, cols)
         dist.reduce_scatter_tensor(red.view(-1), planes.view(-1), group=self.group)
         return red, 1, 0
 

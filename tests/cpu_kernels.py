@@ -116,7 +116,7 @@ def sum_planes(y, x, n, nplanes, plane_stride, accumulate=False):
     s = sum(x.reshape(-1)[p * plane_stride:p * plane_stride + n].double() for p in range(nplanes))
     if accumulate:
         s = s + y.reshape(-1)[:n].double()
-    y.reshape(-1)[:n].copy_(s.float())
+    y.reshape(-1)[:n].copy_(s.float())  # x may be bf16 (partials), y is fp32
 
 
 def axpy(y, x, alpha=1.0):
