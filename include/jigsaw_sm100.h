@@ -63,6 +63,15 @@ typedef struct jg_bcast {
   int32_t n;
 } jg_bcast;
 
+/* Learning-rate schedule of one lr class: linear warm-up from warm_start to
+ * base_lr over warmup_steps (epoch 1), then cosine annealing to final_lr at step total_steps-1.
+ * total_steps <= 0: constant base_lr. */
+#define JG_MAX_LR_CLASSES 4
+typedef struct jg_lr_schedule {
+  float base_lr, warm_start, final_lr;
+  int64_t warmup_steps, total_steps;
+} jg_lr_schedule;
+
 /*
  * jg_gemm — one (batched) GEMM with a fused epilogue.
  * Replaces tensor.matmul (tensor.py:59-72) as called by MpContext._mm (parallel.py:65-69),
@@ -212,12 +221,19 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
  */
 int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n,
             float lr, float beta1, float beta2, float eps, const int32_t* step_dev,
-            const float* grad_scale_dev, void* stream);
+            const float* grad_scale_dev, const float* lr_dev, void* stream);   /* lr_dev != NULL overrides lr */
 /* *counter += 1 on the device (advances the Adam step inside a graph). */
 int jg_step_increment(int32_t* counter, void* stream);
 
-/* Sum of squares of x (fp32) added into out[0] (global grad norm). */
-int jg_sqnorm(const float* x, int64_t n, float* out, void* stream);
+/* weight * (sum of squares of x) added into out[0] (global grad norm; weight
+ * 1/k counts a vector duplicated on k ranks once, parallel.py:483-485). */
+int jg_sqnorm(const float* x, int64_t n, float weight, float* out, void* stream);
+
+/* Device-side optimiser schedule for a captured step: lr_out[i] = lr_at(*step_dev - 1, sched[i])
+ * and, when clip_norm > 0, *grad_scale_out = min(1, clip_norm / sqrt(*sqsum_dev))
+ * (global-norm clipping). Feeds jg_adam's lr_dev / grad_scale_dev. */
+int jg_opt_schedule(const int32_t* step_dev, const jg_lr_schedule* sched, int32_t nsched, const float* sqsum_dev,
+                    float clip_norm, float* lr_out, float* grad_scale_out, void* stream);
 
 /* Introspection. */
 const char* jg_version(void);

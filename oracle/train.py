@@ -6,6 +6,7 @@ to SPEC's worked examples only (tests/test_oracle.py):
   weighted_mse_loss      SPEC.md:401-407  mean of lat_w * var_w * (pred - target)^2
   adam_step              SPEC.md:482-490  bias-corrected Adam, betas (0.9, 0.999), eps 1e-8
   clip_grads
+  lr_at                  SPEC.md:464-472  linear warm-up from 1e-6 over epoch 1, cosine to 1e-5
 Conventions fixed here (stated in DESIGN.md): the mean runs over B x lat_real x lon x C_real;
 zero-padded rows (721 -> 728) and channels get weight 0; p -= lr * mhat / (sqrt(vhat) + eps).
 """
@@ -59,3 +60,14 @@ def clip_grads(grads, clip_norm):
     if norm > clip_norm:
         return [g * (clip_norm / norm) for g in grads], norm
     return list(grads), norm
+
+
+def lr_at(step, total_steps, warmup_steps, base=1e-4, warm_start=1e-6, final=1e-5):
+    """SPEC lr_at: linear from warm_start to base across the warm-up (epoch 1), then
+    final + (base - final) / 2 * (1 + cos(pi t)), t = progress through the remaining steps."""
+    if not 0 <= step < total_steps:
+        raise ValueError("step out of range")
+    if step < warmup_steps:
+        return warm_start + (base - warm_start) * step / warmup_steps
+    t = (step - warmup_steps) / max(1, total_steps - 1 - warmup_steps)
+    return final + (base - final) / 2.0 * (1.0 + np.cos(np.pi * t))

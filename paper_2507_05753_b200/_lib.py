@@ -34,8 +34,9 @@ EXPORTED = [
     "jg_ln_moments", "jg_ln_apply", "jg_ln_bwd_moments", "jg_ln_bwd_apply",
     "jg_colsum", "jg_rowsum", "jg_patchify", "jg_unpatchify", "jg_blend_loss",
     "jg_adam", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async",
-    "jg_version", "jg_last_error", "jg_launch_count",
+    "jg_opt_schedule", "jg_version", "jg_last_error", "jg_launch_count",
 ]
+JG_MAX_LR_CLASSES = 4
 
 
 class Bcast(ctypes.Structure):
@@ -53,6 +54,12 @@ def make_bcast(addrs) -> "Bcast | None":
         b.ptr[i] = a
     b.n = len(addrs)
     return b
+
+
+class LrSchedule(ctypes.Structure):
+    """jg_lr_schedule (SPEC.md:464-472)."""
+    _fields_ = [("base_lr", ctypes.c_float), ("warm_start", ctypes.c_float), ("final_lr", ctypes.c_float),
+                ("warmup_steps", ctypes.c_int64), ("total_steps", ctypes.c_int64)]
 
 
 class GemmDesc(ctypes.Structure):
@@ -109,9 +116,10 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_patchify": [vp, vp, i32, i64, i64, i64, i64, i64, i64, vp],
         "jg_unpatchify": [vp, vp, i64, i64, i64, i64, i64, i64, vp],
         "jg_blend_loss": [vp] * 12 + [i64] * 6 + [f32, f32, vp, vp],
-        "jg_adam": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp],
+        "jg_adam": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp, vp],
         "jg_step_increment": [vp, vp],
-        "jg_sqnorm": [vp, i64, vp, vp],
+        "jg_sqnorm": [vp, i64, f32, vp, vp],
+        "jg_opt_schedule": [vp, ctypes.POINTER(LrSchedule), i32, vp, f32, vp, vp, vp],
         "jg_epilogue": [ctypes.POINTER(GemmDesc), vp, i32, i64, i64, i32, vp],
         "jg_axpy": [vp, vp, f32, i64, vp],
         "jg_sum_planes": [vp, vp, i32, i64, i32, i64, i32, vp],

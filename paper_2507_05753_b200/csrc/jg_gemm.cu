@@ -112,6 +112,20 @@ __device__ __forceinline__ void stage_store(uint8_t* stg, const float* v, bool b
   }
 }
 
+// L2-aware tile order: tiles run m-fastest inside groups of TILE_GROUP_M row tiles, so one wave of
+// ~148 CTAs covers a ~8 x (units/8) block of the output and reads ~8 + units/8 operand panels per
+// k-step from DRAM instead of (units / n_tiles) + n_tiles (long-K token GEMMs: B re-read per wave).
+constexpr int TILE_GROUP_M = 8;
+__device__ __forceinline__ void tile_coords(int rem, int m_tiles, int n_tiles, int& mi, int& ni) {
+  const int per_group = TILE_GROUP_M * n_tiles;
+  const int g = rem / per_group;
+  const int first = g * TILE_GROUP_M;
+  const int gm = min(TILE_GROUP_M, m_tiles - first);
+  const int r = rem - g * per_group;
+  mi = first + r % gm;
+  ni = r / gm;
+}
+
 template <int BN, bool TF32, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
   using C = Cfg<BN, TF32, CG>;
@@ -173,8 +187,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
       const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
       const int rem = tile - tb * tiles_per_batch;
-      const int m0 = (rem / p.n_tiles) * (BM * CG) + BM * static_cast<int>(cta_rank);
-      const int n0 = (rem % p.n_tiles) * BN + (BN / CG) * static_cast<int>(cta_rank);
+      int mi, ni;
+      tile_coords(rem, p.m_tiles, p.n_tiles, mi, ni);
+      const int m0 = mi * (BM * CG) + BM * static_cast<int>(cta_rank);
+      const int n0 = ni * BN + (BN / CG) * static_cast<int>(cta_rank);
       for (int seg = 0; seg < p.nseg; ++seg) {
         for (int bb = 0; bb < kb_batches; ++bb) {
           const int b = p.reduce_batch ? bb : tb;
@@ -270,8 +286,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
       const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
       const int rem = tile - tb * tiles_per_batch;
-      const int m0 = (rem / p.n_tiles) * (BM * CG) + BM * static_cast<int>(cta_rank);
-      const int n0 = (rem % p.n_tiles) * BN;
+      int mi, ni;
+      tile_coords(rem, p.m_tiles, p.n_tiles, mi, ni);
+      const int m0 = mi * (BM * CG) + BM * static_cast<int>(cta_rank);
+      const int n0 = ni * BN;
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < p.m;
       jgd::mbar_wait(&tfull[acc], acc_phase);

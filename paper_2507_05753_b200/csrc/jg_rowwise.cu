@@ -445,8 +445,10 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
 // ---------------------------------------------------------------- Adam
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, __nv_bfloat16* __restrict__ pb, int64_t n, float lr, float b1,
-                            float b2, float eps, const int32_t* __restrict__ step, const float* __restrict__ gscale) {
+                            float b2, float eps, const int32_t* __restrict__ step, const float* __restrict__ gscale,
+                            const float* __restrict__ lr_dev) {
   const int t = *step;
+  if (lr_dev) lr = *lr_dev;
   const float bc1 = 1.0f / (1.0f - powf(b1, (float)t));
   const float bc2 = 1.0f / (1.0f - powf(b2, (float)t));
   const float s = gscale ? *gscale : 1.0f;
@@ -487,12 +489,21 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
 
 __global__ void step_inc_kernel(int32_t* counter) { *counter += 1; }
 
-__global__ void sqnorm_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+__global__ void sqnorm_kernel(const float* __restrict__ x, int64_t n, float weight, float* __restrict__ out,
+                              bool vec) {
   __shared__ float part[32];
   float s = 0.f;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = x[i];
-    s += v * v;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 4; i += stride) {
+      const float4 v = reinterpret_cast<const float4*>(x)[i];
+      s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+      const float v = x[i];
+      s += v * v;
+    }
   }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
@@ -500,7 +511,37 @@ __global__ void sqnorm_kernel(const float* __restrict__ x, int64_t n, float* __r
   if (threadIdx.x < 32) {
     float v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
     v = warp_sum(v);
-    if (threadIdx.x == 0) atomicAdd(out, v);
+    if (threadIdx.x == 0) atomicAdd(out, v * weight);
+  }
+}
+
+// lr_at for each lr class, evaluated at optimiser step *step - 1, and the
+// global-norm clip factor from the summed squares.
+struct SchedArgs { jg_lr_schedule s[JG_MAX_LR_CLASSES]; int n; };
+
+__device__ float lr_at_dev(const jg_lr_schedule& c, int64_t step) {
+  if (c.total_steps <= 0) return c.base_lr;  // no schedule: constant lr
+  if (step < 0) step = 0;
+  if (step > c.total_steps - 1) step = c.total_steps - 1;
+  if (step < c.warmup_steps)
+    return c.warm_start + (c.base_lr - c.warm_start) * (float)((double)step / (double)c.warmup_steps);
+  const int64_t span = c.total_steps - 1 - c.warmup_steps;
+  const double u = span > 0 ? (double)(step - c.warmup_steps) / (double)span : 1.0;
+  return (float)(c.final_lr + 0.5 * ((double)c.base_lr - c.final_lr) * (1.0 + cos(3.14159265358979323846 * u)));
+}
+
+__global__ void opt_schedule_kernel(const int32_t* __restrict__ step, const SchedArgs a, const float* __restrict__ sq,
+                                    float clip, float* __restrict__ lr_out, float* __restrict__ gscale) {
+  if (threadIdx.x != 0) return;
+  const int64_t t = (int64_t)(*step) - 1;
+  for (int i = 0; i < a.n; ++i) lr_out[i] = lr_at_dev(a.s[i], t);
+  if (gscale) {
+    float f = 1.0f;
+    if (clip > 0.f && sq) {
+      const float norm = sqrtf(*sq);
+      if (norm > clip) f = clip / norm;
+    }
+    *gscale = f;
   }
 }
 
@@ -829,14 +870,31 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
 }
 
 int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, float lr, float beta1, float beta2,
-            float eps, const int32_t* step_dev, const float* grad_scale_dev, void* stream) {
+            float eps, const int32_t* step_dev, const float* grad_scale_dev, const float* lr_dev, void* stream) {
   JG_SHAPE_CHECK(n >= 0 && step_dev, "jg_adam: bad arguments");
   JG_SHAPE_CHECK(al16(p) && al16(g) && al16(m) && al16(v) && (!p_bf16 || (reinterpret_cast<uintptr_t>(p_bf16) & 7u) == 0),
                  "jg_adam: buffers must be 16B aligned");
   if (n == 0) return JG_OK;
   adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
-      p, g, m, v, (__nv_bfloat16*)p_bf16, n, lr, beta1, beta2, eps, step_dev, grad_scale_dev);
+      p, g, m, v, (__nv_bfloat16*)p_bf16, n, lr, beta1, beta2, eps, step_dev, grad_scale_dev, lr_dev);
   JG_LAUNCH_CHECK("adam");
+  return JG_OK;
+}
+
+int jg_opt_schedule(const int32_t* step_dev, const jg_lr_schedule* sched, int32_t nsched, const float* sqsum_dev,
+                    float clip_norm, float* lr_out, float* grad_scale_out, void* stream) {
+  JG_SHAPE_CHECK(step_dev && nsched >= 0 && nsched <= JG_MAX_LR_CLASSES && (nsched == 0 || (sched && lr_out)),
+                 "jg_opt_schedule: bad arguments");
+  JG_SHAPE_CHECK(clip_norm <= 0.f || (sqsum_dev && grad_scale_out), "jg_opt_schedule: clipping needs sqsum and scale");
+  SchedArgs a{};
+  a.n = nsched;
+  for (int i = 0; i < nsched; ++i) {
+    JG_SHAPE_CHECK(sched[i].total_steps <= 0 || (sched[i].warmup_steps >= 0 && sched[i].warmup_steps < sched[i].total_steps),
+                   "jg_opt_schedule: warm-up must end before the last step");
+    a.s[i] = sched[i];
+  }
+  opt_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(step_dev, a, sqsum_dev, clip_norm, lr_out, grad_scale_out);
+  JG_LAUNCH_CHECK("opt_schedule");
   return JG_OK;
 }
 
@@ -846,9 +904,10 @@ int jg_step_increment(int32_t* counter, void* stream) {
   return JG_OK;
 }
 
-int jg_sqnorm(const float* x, int64_t n, float* out, void* stream) {
+int jg_sqnorm(const float* x, int64_t n, float weight, float* out, void* stream) {
   if (n == 0) return JG_OK;
-  sqnorm_kernel<<<grid_for(n, 1024), 256, 0, (cudaStream_t)stream>>>(x, n, out);
+  const bool vec = n % 4 == 0 && al16(x);
+  sqnorm_kernel<<<grid_for(vec ? n / 4 : n, 256), 256, 0, (cudaStream_t)stream>>>(x, n, weight, out, vec);
   JG_LAUNCH_CHECK("sqnorm");
   return JG_OK;
 }

@@ -16,6 +16,7 @@ import torch
 
 from . import _lib
 from . import kernels as K
+from .errors import ConfigError
 from .model import WeatherMixerModel
 from .train import AdamConfig
 
@@ -32,11 +33,20 @@ class TrainStep:
         self.overwrite = r == 1
         self.fused_adam = fused_adam and r == 1 and (model.ctx.n == 1 or batch == 1)
         self.adam = adam or AdamConfig()
+        a = self.adam
+        self.clip = float(a.clip_norm) if a.clip_norm is not None and a.clip_norm > 0 else None
+        self.scheduled = a.total_steps > 0
+        if self.fused_adam and (self.clip is not None or model.ctx.dp_replicas > 1):
+            raise ConfigError("fused_adam applies Adam inside the gradient GEMMs; clipping and dp_reduce "
+                              "need the whole gradient first")
         self.loss_scale = loss_scale
         self.ws = model.workspace(batch, r)
         dev = model.device
         self.target = torch.zeros_like(self.ws.xin)
         self.step_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.lr_dev = torch.zeros(_lib.JG_MAX_LR_CLASSES, dtype=torch.float32, device=dev)  # this step's lr per class
+        self.grad_scale = torch.ones(1, dtype=torch.float32, device=dev)                # clip factor
+        self.sqsum = torch.zeros(1, dtype=torch.float32, device=dev)                    # global squared grad norm
         self.use_graph = graph
         self.graph = None
         self.launches_per_step = None
@@ -76,18 +86,39 @@ class TrainStep:
             m._fused_adam = None
             m._grad_overwrite = False
         m.grad_sync()
+        m.ctx.all_reduce_dp_mean(m.flat.grad)  # dp_reduce over replicas of this shard (no-op for one)
+        if self.clip is not None:
+            self._global_sqnorm()
+        if self.clip is not None or self.scheduled:
+            K.opt_schedule(self.step_count, [self.adam.schedule(c) for c in m.flat.CLASSES], self.sqsum, self.clip,
+                           self.lr_dev, self.grad_scale)
         self._adam()
+
+    def _global_sqnorm(self) -> None:
+        """Squared L2 norm of the global gradient: local shards summed over the
+        mp group, duplicated vectors counted once (weight 1/R for column vectors shared by the
+        column group, 1/C for the row vector shared by the row group; parallel.py:483-485)."""
+        m, f = self.model, self.model.flat
+        self.sqsum.zero_()
+        for cls in f.CLASSES:
+            for kind, w in (("matrix", 1.0), ("vec_col", 1.0 / m.R), ("vec_row", 1.0 / m.C)):
+                lo, hi = f.kind_range[(cls, kind)]
+                if hi > lo:
+                    K.sqnorm(f.grad[lo:hi], self.sqsum, w)
+        m.ctx.all_reduce_all(self.sqsum)
 
     def _adam(self) -> None:
         f, a = self.model.flat, self.adam
         op_copy = f.op if f.op is not f.master else None
-        for cls, (lo, hi) in f.class_range.items():
+        for i, (cls, (lo, hi)) in enumerate(f.class_range.items()):
             if self.fused_adam:
                 lo, hi = f.vec_range(cls)
             if hi <= lo:
                 continue
             K.adam(f.master[lo:], f.grad[lo:], f.m[lo:], f.v[lo:], None if op_copy is None else op_copy[lo:],
-                   hi - lo, a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count)
+                   hi - lo, a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count,
+                   grad_scale=self.grad_scale if self.clip is not None else None,
+                   lr_dev=self.lr_dev[i:i + 1] if self.scheduled else None)
 
     def capture(self) -> None:
         """Warm up on a side stream, then capture the step into two CUDA graphs (forward | loss +

@@ -113,9 +113,24 @@ def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blen
               batch, lat, lon, chans, pl, pw, float(inv_count), float(loss_scale), _bref(bcast))
 
 
-def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None):
+def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None):
+    """jg_adam; lr_dev (device float, e.g. one entry of the schedule's output) overrides lr."""
     _lib.call("jg_adam", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), ptr(p_op), n, float(lr),
-              float(beta1), float(beta2), float(eps), step.data_ptr(), ptr(grad_scale))
+              float(beta1), float(beta2), float(eps), step.data_ptr(), ptr(grad_scale), ptr(lr_dev))
+
+
+def sqnorm(x, out, weight=1.0, n=None):
+    """out[0] += weight * sum(x[:n]^2) (fp32)."""
+    _lib.call("jg_sqnorm", x.data_ptr(), x.numel() if n is None else n, float(weight), out.data_ptr())
+
+
+def opt_schedule(step, scheds, sqsum, clip_norm, lr_out, grad_scale):
+    """jg_opt_schedule: per-class lr of this step (device) and the global-norm clip factor."""
+    arr = (_lib.LrSchedule * max(1, len(scheds)))()
+    for i, s in enumerate(scheds):
+        arr[i] = _lib.LrSchedule(*s)
+    _lib.call("jg_opt_schedule", step.data_ptr(), arr, len(scheds), ptr(sqsum), float(clip_norm or 0.0),
+              ptr(lr_out), ptr(grad_scale))
 
 
 def step_increment(counter):

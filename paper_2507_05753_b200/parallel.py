@@ -57,8 +57,18 @@ class MpContext:
         self.col_ranks = [group[i * self.C + self.c] for i in range(self.R)]
         self.row_group = self.col_group = None
         self.mp_group = None
+        self.dp_group = None
+        pg = ProcessGroup(comm.world_size, self.n, comm.rank) if comm.world_size % self.n == 0 else None
+        self.dp_replicas = pg.dp_replicas if pg is not None else 1
+        self.dp_index = pg.dp_index if pg is not None else 0
         if self.n > 1:
             self._build_groups()
+        if self.dp_replicas > 1:
+            # dp groups {r : r % n == c} (comm.py:346-361), created in the same order on every rank
+            for ranks in ProcessGroup.dp_groups(comm.world_size, self.n):
+                g = comm.group(ranks)
+                if comm.rank in ranks:
+                    self.dp_group = g
 
     def _build_groups(self) -> None:
         # new_group is collective over the whole world: every rank creates every mp group's row
@@ -145,6 +155,14 @@ class MpContext:
     def all_reduce_all(self, x: torch.Tensor) -> torch.Tensor:
         if self.n > 1:
             dist.all_reduce(x, group=self.mp_group)
+        return x
+
+    def all_reduce_dp_mean(self, x: torch.Tensor) -> torch.Tensor:
+        """dp_reduce: mean of this shard's gradient over the replicas holding
+        the same shard; a no-op for a single replica."""
+        if self.dp_replicas > 1:
+            dist.all_reduce(x, group=self.dp_group)
+            x.mul_(1.0 / self.dp_replicas)
         return x
 
     def all_reduce_row(self, x: torch.Tensor) -> torch.Tensor:

@@ -106,7 +106,6 @@ class SymmTransport:
     kind = "symm"
 
     def __init__(self, group, G: int, idx: int, device, scratch_bytes: int, persist_spec):
-        import torch.distributed._symmetric_memory as symm
         self.group, self.G, self.idx, self.device = group, G, idx, device
         self.offsets: dict[str, tuple[int, tuple, torch.dtype]] = {}
         off = 0
@@ -118,16 +117,20 @@ class SymmTransport:
             off += -(-n * torch.empty((), dtype=dtype).element_size() // 256) * 256
         self.scratch_off = off
         self.scratch_bytes = -(-scratch_bytes // 256) * 256
-        total = off + 2 * self.scratch_bytes
-        name = group.group_name
+        self.k = 0
+        self._alloc(off + 2 * self.scratch_bytes)
+
+    def _alloc(self, total: int) -> None:
+        """One symmetric arena per group member; self.base[j] = member j's arena address."""
+        import torch.distributed._symmetric_memory as symm
+        name = self.group.group_name
         try:
             symm.enable_symm_mem_for_group(name)
         except Exception:  # noqa: BLE001  (newer torch enables on demand)
             pass
-        self.buf = symm.empty(total, dtype=torch.uint8, device=device)
+        self.buf = symm.empty(total, dtype=torch.uint8, device=self.device)
         self.hdl = symm.rendezvous(self.buf, name)
         self.base = [int(p) for p in self.hdl.buffer_ptrs]
-        self.k = 0
 
     def reserve(self, name, shape, dtype):  # persistent slots are fixed at construction
         assert name in self.offsets, name

@@ -21,6 +21,37 @@ def _view(t, size, stride, extra=0):
     return torch.as_strided(t, size, stride, t.storage_offset() + extra)
 
 
+# ---- emulated peer memory (tests/shm_transport.py): raw "device addresses" handed out by the
+# transport are synthetic; they resolve to shared-file arenas mapped in every rank's process.
+_PEERS: list = []
+
+
+def register_peer(base: int, buf: torch.Tensor) -> None:
+    _PEERS.append((base, buf.numel(), buf))
+
+
+def _at(addr: int, dtype, size, stride):
+    es = torch.empty((), dtype=dtype).element_size()
+    span = 1 + sum((a - 1) * b for a, b in zip(size, stride))
+    for base, n, buf in _PEERS:
+        if base <= addr < base + n:
+            off = addr - base
+            assert off % es == 0 and off + span * es <= n, (addr, base, n, span)
+            return torch.as_strided(buf[off:off + span * es].view(dtype), size, stride)
+    raise AssertionError(f"address {addr:#x} is not in any emulated peer arena")
+
+
+def _bcast_copy(src, addrs):
+    """Store the just-written output `src` (a strided view) at every peer address too."""
+    for a in addrs or []:
+        _at(a, src.dtype, tuple(src.shape), tuple(src.stride())).copy_(src)
+
+
+def copy_async(dst_ptr, src, nbytes=None):
+    nbytes = src.numel() * src.element_size() if nbytes is None else nbytes
+    _at(dst_ptr, torch.uint8, (nbytes,), (1,)).copy_(src.contiguous().view(-1).view(torch.uint8)[:nbytes])
+
+
 def _gelu(x):
     return x * 0.5 * (1.0 + torch.erf(x / math.sqrt(2.0)))
 
@@ -57,7 +88,6 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
          bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
          d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None, d_planes=None, d_bcast=None,
          d2_bcast=None):
-    assert d_planes is None and not d_bcast and not d2_bcast, "the CPU double has no peer memory"
     lda = lda if lda is not None else (k if am == KM else m)
     ldb = ldb if ldb is not None else (k if bm == KM else n)
     ldd = ldd if ldd is not None else n
@@ -91,16 +121,26 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
             if apb is not None:
                 _view(apb, (m, n), (ldd, 1), ob * d_bs).copy_(w.to(apb.dtype))
         return out
+    if d_planes:  # fused reduce-scatter: batch ob's partial goes straight to its owner's plane
+        assert epi == 0 and len(d_planes) >= len(acc)
+        for ob, v in enumerate(acc):
+            _at(d_planes[ob], out.dtype, (m, n), (ldd, 1)).copy_((v * alpha).to(out.dtype))
+        return out
     for ob, v in enumerate(acc):
         _apply_epilogue(v, ob, m, n, epi, alpha, out, ldd, d_bs, d2, n, d2_bs, bias, bias_bs, resid, n, r_bs,
                         pre, n, p_bs, stats, stats_bs)
+    if d_bcast or d2_bcast:
+        assert len(acc) == 1
+        _bcast_copy(_view(out, (m, n), (ldd, 1)), d_bcast)
+        if d2 is not None:
+            _bcast_copy(_view(d2, (m, n), (n, 1)), d2_bcast)
     return out
 
 
 def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alpha=1.0, d=None, ldd=None, d_bs=0,
              d2=None, ldd2=None, d2_bs=0, bias=None, bias_bs=0, resid=None, ldr=None, r_bs=0, pre=None, ldp=None,
              p_bs=0, stats=None, stats_bs=0, d_bcast=None, d2_bcast=None):
-    assert not d_bcast and not d2_bcast
+    assert batch == 1 or not (d_bcast or d2_bcast)
     acc_ld = acc_ld if acc_ld is not None else n
     for ob in range(batch):
         if nplanes > 1:
@@ -110,6 +150,10 @@ def epilogue(acc, m, n, *, batch=1, acc_ld=None, acc_bs=0, nplanes=1, epi=0, alp
         _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd if ldd is not None else n, d_bs, d2,
                         ldd2 if ldd2 is not None else n, d2_bs, bias, bias_bs, resid, ldr if ldr is not None else n,
                         r_bs, pre, ldp if ldp is not None else n, p_bs, stats, stats_bs)
+    if d_bcast:
+        _bcast_copy(_view(d, (m, n), (ldd if ldd is not None else n, 1)), d_bcast)
+    if d2_bcast:
+        _bcast_copy(_view(d2, (m, n), (ldd2 if ldd2 is not None else n, 1)), d2_bcast)
 
 
 def sum_planes(y, x, n, nplanes, plane_stride, accumulate=False):
@@ -144,7 +188,6 @@ def ln_moments(x, stats, rows, cols):
 
 
 def ln_apply(x, stats, gamma, beta, y, mean_rstd, rows, cols, c_total, eps, bcast=None):
-    assert not bcast
     st = stats.reshape(rows, 2).double()
     mean = st[:, 0] / c_total
     var = st[:, 1] / c_total - mean * mean
@@ -153,6 +196,7 @@ def ln_apply(x, stats, gamma, beta, y, mean_rstd, rows, cols, c_total, eps, bcas
         mean_rstd.reshape(rows, 2).copy_(torch.stack([mean, rstd], 1).float())
     xv = x.reshape(rows, cols).double()
     y.reshape(rows, cols).copy_((gamma.double() * (xv - mean[:, None]) * rstd[:, None] + beta.double()).to(y.dtype))
+    _bcast_copy(y.reshape(rows, cols), bcast)
 
 
 def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
@@ -166,7 +210,6 @@ def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
 
 def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total,
                  bcast=None):
-    assert not bcast
     mr = mean_rstd.reshape(rows, 2).double()
     xh = (x.reshape(rows, cols).double() - mr[:, :1]) * mr[:, 1:]
     gv = g.reshape(rows, cols).double()
@@ -178,6 +221,8 @@ def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbe
     out.reshape(rows, cols).copy_(dx.to(out.dtype))
     if out_op is not None and out_op is not out:
         out_op.reshape(rows, cols).copy_(dx.to(out_op.dtype))
+    if bcast:
+        _bcast_copy((out_op if out_op is not None else out).reshape(rows, cols), bcast)
     if dgamma is not None:
         dgamma += (gv * xh).sum(0).float()
     if dbeta is not None:
@@ -194,7 +239,6 @@ def rowsum(x, out, rows, cols, ld=None):
 
 def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blend, g_dec, batch, lat, lon, chans,
                pl, pw, inv_count, loss_scale, bcast=None):
-    assert not bcast
     decoded = _unpatchify(dec.double(), batch, lat, lon, chans, pl, pw)
     x = xin.double()
     w = blend_w.double()
@@ -217,10 +261,41 @@ def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blen
         gd = gout * w
         t = gd.reshape(batch, lat // pl, pl, lon // pw, pw, chans).permute(0, 1, 3, 5, 2, 4)
         g_dec.copy_(t.reshape(g_dec.shape).to(g_dec.dtype))
+        _bcast_copy(g_dec, bcast)
 
 
-def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None):
+def sqnorm(x, out, weight=1.0, n=None):
+    xv = x.reshape(-1)[: x.numel() if n is None else n].double()
+    out += float(weight) * float((xv * xv).sum())
+
+
+def opt_schedule(step, scheds, sqsum, clip_norm, lr_out, grad_scale):
+    t = int(step.item()) - 1
+    for i, (base, warm, final, wsteps, total) in enumerate(scheds):
+        if total <= 0:
+            lr = base
+        else:
+            s_ = min(max(t, 0), total - 1)
+            if s_ < wsteps:
+                lr = warm + (base - warm) * s_ / wsteps
+            else:
+                span = total - 1 - wsteps
+                u = (s_ - wsteps) / span if span > 0 else 1.0
+                lr = final + 0.5 * (base - final) * (1 + math.cos(math.pi * u))
+        lr_out[i] = lr
+    if grad_scale is not None:
+        f = 1.0
+        if clip_norm and clip_norm > 0:
+            norm = math.sqrt(float(sqsum.item()))
+            if norm > clip_norm:
+                f = clip_norm / norm
+        grad_scale.fill_(f)
+
+
+def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None):
     t = int(step.item())
+    if lr_dev is not None:
+        lr = float(lr_dev.item())
     pv, gv, mv, vv = p.reshape(-1)[:n], g.reshape(-1)[:n], m.reshape(-1)[:n], v.reshape(-1)[:n]
     s = float(grad_scale.item()) if grad_scale is not None else 1.0
     gg = gv * s
@@ -236,7 +311,8 @@ def step_increment(counter):
 
 
 NAMES = ["gemm", "epilogue", "sum_planes", "axpy", "cast_bf16", "patchify", "ln_moments", "ln_apply", "ln_bwd_moments",
-         "ln_bwd_apply", "colsum", "rowsum", "blend_loss", "adam", "step_increment"]
+         "ln_bwd_apply", "colsum", "rowsum", "blend_loss", "adam", "step_increment", "sqnorm", "opt_schedule",
+         "copy_async"]
 
 
 def install():

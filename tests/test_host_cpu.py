@@ -165,3 +165,38 @@ def test_product_comm_volume_matches_reference_tables():
         rep = comm_volume(int(m), int(k), int(no), int(n), mode, batch=int(b[1:]))
         assert (rep.forward_sent, rep.backward_sent) == (fwd, bwd), key
         assert rep.total_sent == sum(fwd) + sum(bwd) == rep.total_received
+
+
+def test_lr_schedule_spec_examples():
+    """step 0 -> 1e-6, end of epoch 1 -> 1e-4 (body), last step -> 1e-5; the
+    warm-up end equals the cosine start; host mirror == oracle restatement; out-of-range raises."""
+    import math
+    from oracle import train as ot
+    from paper_2507_05753_b200.train import AdamConfig
+    a = AdamConfig(warmup_steps=100, total_steps=10000)
+    assert math.isclose(a.lr_at(0), 1e-6)
+    assert math.isclose(a.lr_at(100), 1e-4)
+    assert math.isclose(a.lr_at(9999), 1e-5)
+    assert math.isclose(a.lr_at(9999, "encdec"), 2e-6)
+    assert abs(a.lr_at(99) - a.lr_at(100)) < 1e-6  # continuous across the warm-up end
+    for s in (0, 1, 50, 99, 100, 101, 5000, 9998, 9999):
+        assert math.isclose(a.lr_at(s), ot.lr_at(s, 10000, 100), rel_tol=1e-12)
+    with pytest.raises(ValueError):
+        a.lr_at(10000)
+    assert AdamConfig().lr_at(123, "encdec") == 2e-5  # no schedule: constant class lr
+
+
+def test_clip_spec_examples():
+    from oracle import train as ot
+    g, norm = ot.clip_grads([np.array([3.0, 4.0])], 1.0)
+    assert np.allclose(g[0], [0.6, 0.8]) and norm == 5.0
+    g, _ = ot.clip_grads([np.array([0.3, 0.4])], 1.0)
+    assert np.allclose(g[0], [0.3, 0.4])
+
+
+def test_dp_groups_rule():
+    """SPEC.md:491-499 examples: n=2 in 8 ranks -> {0,2,4,6},{1,3,5,7}; n=4 -> {0,4},..."""
+    from paper_2507_05753_b200.comm import ProcessGroup
+    assert ProcessGroup.dp_groups(8, 2) == [[0, 2, 4, 6], [1, 3, 5, 7]]
+    assert ProcessGroup.dp_groups(8, 4) == [[0, 4], [1, 5], [2, 6], [3, 7]]
+    assert ProcessGroup(4, 4, 1).dp_replicas == 1

@@ -28,7 +28,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out_q, r, mode="fwdbwd"):
+def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
     try:
         import sys
         sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -38,12 +38,18 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd"):
         torch.set_num_threads(1)
         import cpu_kernels
         cpu_kernels.install()
+        if (opts or {}).get("transport") == "shm":
+            import shm_transport
+            shm_transport.install()
         from oracle import model as om
         from paper_2507_05753_b200 import Communicator, ModelConfig, MpContext, WeatherMixerModel
         z = np.load(os.path.join(GOLD, "wm_golden.npz"))
         meta = json.load(open(os.path.join(GOLD, "comm_golden.json")))
         comm = Communicator.from_env(backend="gloo") if world > 1 else Communicator.local()
-        ctx = MpContext(comm, list(range(world)))
+        opts = opts or {}
+        n_mp = opts.get("mp", world)
+        k = rank // n_mp
+        ctx = MpContext(comm, list(range(k * n_mp, (k + 1) * n_mp)))
         cfg = ModelConfig.from_dict(meta["config"])
         model = WeatherMixerModel(ctx, cfg, seed=0, dtype="f32", device="cpu")
         oc = om.Config(**{**meta["config"], "grid": tuple(meta["config"]["grid"]), "patch": tuple(meta["config"]["patch"])})
@@ -53,15 +59,21 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd"):
         gl = om.local_sample(oc, g, ctx.R, ctx.C, ctx.r, ctx.c)
         if mode == "train":
             from paper_2507_05753_b200.engine import TrainStep
-            tl = om.local_sample(oc, z["g_out"][:1] * 0.5, ctx.R, ctx.C, ctx.r, ctx.c)  # a target
-            step = TrainStep(model, batch=1, graph=False)
-            losses = []
-            for _ in range(2):
+            from paper_2507_05753_b200.train import AdamConfig
+            si = opts.get("sample", lambda kk: 0)(k) if callable(opts.get("sample")) else (k if opts.get("dp") else 0)
+            xl = om.local_sample(oc, z["x"][si:si + 1], ctx.R, ctx.C, ctx.r, ctx.c)
+            tl = om.local_sample(oc, z["g_out"][si:si + 1] * 0.5, ctx.R, ctx.C, ctx.r, ctx.c)  # a target
+            step = TrainStep(model, batch=1, graph=False, adam=AdamConfig(**opts.get("adam", {})))
+            losses, scales, lrs = [], [], []
+            for _ in range(opts.get("steps", 2)):
                 step.ws.xin.copy_(torch.tensor(xl[:1], dtype=torch.float32))
                 step.target.copy_(torch.tensor(tl, dtype=torch.float32))
                 step._body()
                 losses.append(float(step.ws.loss.item()))
-            res = {"pos": ctx.pos, "rc": (ctx.R, ctx.C, ctx.r, ctx.c), "losses": losses,
+                scales.append(float(step.grad_scale.item()))
+                lrs.append(step.lr_dev[:2].tolist())
+            res = {"pos": ctx.pos, "rank": rank, "rc": (ctx.R, ctx.C, ctx.r, ctx.c), "losses": losses,
+                   "scales": scales, "lrs": lrs,
                    "params": {k: p.data.numpy().copy() for k, p in model.params.items()}}
             out_q.put(res)
             if world > 1:
@@ -73,6 +85,9 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd"):
         out = model.forward(torch.tensor(xl, dtype=torch.float32), r=r)
         model.backward(torch.tensor(gl, dtype=torch.float32))
         model.grad_sync()
+        if opts.get("transport") == "shm":
+            g = model._ws.grid
+            assert type(g.row if g.row is not None else g.col).__name__ == "ShmSymmTransport"
         res = {"pos": ctx.pos, "out": out.numpy(), "grads": {k: p.grad.numpy().copy() for k, p in model.params.items()},
                "rc": (ctx.R, ctx.C, ctx.r, ctx.c)}
         out_q.put(res)
@@ -84,11 +99,11 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd"):
         out_q.put({"error": traceback.format_exc(), "rank": rank})
 
 
-def _run(world, r=1, mode="fwdbwd"):
+def _run(world, r=1, mode="fwdbwd", opts=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(rk, world, port, q, r, mode)) for rk in range(world)]
+    procs = [ctx.Process(target=_worker, args=(rk, world, port, q, r, mode, opts)) for rk in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -97,15 +112,15 @@ def _run(world, r=1, mode="fwdbwd"):
     for rr in res:
         if "error" in rr:
             raise AssertionError(f"rank {rr['rank']} failed:\n{rr['error']}")
-    return sorted(res, key=lambda d: d["pos"])
+    return sorted(res, key=lambda d: (d.get("rank", 0), d["pos"]))
 
 
-def _check(world, r=1):
+def _check(world, r=1, opts=None):
     from oracle import model as om
     z = np.load(os.path.join(GOLD, "wm_golden.npz"))
     meta = json.load(open(os.path.join(GOLD, "comm_golden.json")))
     oc = om.Config(**{**meta["config"], "grid": tuple(meta["config"]["grid"]), "patch": tuple(meta["config"]["patch"])})
-    res = _run(world, r)
+    res = _run(world, r, opts=opts)
     out_key = "out_f64" if r == 1 else "rollout_out_f64"
     gpre = "grad_f64/" if r == 1 else "rollout_grad_f64/"
     ref_out = z[out_key]
@@ -131,6 +146,17 @@ def test_jigsaw_grid_matches_reference(world):
 
 def test_jigsaw_rollout_4way():
     _check(4, r=2)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_symmetric_memory_schedule_matches_reference(world):
+    """The peer-memory transport's plumbing (slots, rotating partial regions, producer pushes,
+    epilogue stores into owners' planes, q-way sub-chunks at 4 x 2) on emulated peer memory."""
+    _check(world, opts={"transport": "shm"})
+
+
+def test_symmetric_memory_rollout_8way():
+    _check(8, r=2, opts={"transport": "shm"})
 
 
 @pytest.mark.parametrize("world", [1, 2, 4])
@@ -162,3 +188,121 @@ def test_train_step_fused_adam_matches_oracle(world):
         upd_got = np.concatenate([(d["params"][k] - om.local_tile(oc, k, p0[k], R, C, rr, cc)).ravel() for k in params])
         upd_ref = np.concatenate([(om.local_tile(oc, k, params[k] - p0[k], R, C, rr, cc)).ravel() for k in params])
         assert np.linalg.norm(upd_got - upd_ref) / np.linalg.norm(upd_ref) < 1e-3
+
+
+def _oracle_train(oc, samples, steps, adam_opts=None, clip=None):
+    """Serial f64 training: per step, the mean over `samples` of each sample's gradient (dp_reduce),
+    global-norm clip, scheduled Adam. Returns (per-sample losses per step, params, p0)."""
+    from oracle import model as om, train as ot
+    z = np.load(os.path.join(GOLD, "wm_golden.npz"))
+    params = om.init_params(oc, 0, np.float64)
+    p0 = {k: v.copy() for k, v in params.items()}
+    mom = {k: np.zeros_like(v) for k, v in params.items()}
+    vel = {k: np.zeros_like(v) for k, v in params.items()}
+    a = adam_opts or {}
+    losses, norms = [], []
+    for step in range(1, steps + 1):
+        acc, ls = None, []
+        for si in samples:
+            model = om.SerialModel(oc, params)
+            loss, g = ot.weighted_mse_loss(model.forward(z["x"][si:si + 1]), z["g_out"][si:si + 1] * 0.5,
+                                           ot.lat_weights(oc.grid[0]), np.ones(oc.n_vars))
+            grads = model.backward(g)
+            ls.append(loss)
+            acc = grads if acc is None else {k: acc[k] + grads[k] for k in acc}
+        grads = {k: v / len(samples) for k, v in acc.items()}
+        names = list(grads)
+        clipped, norm = ot.clip_grads([grads[k] for k in names], clip) if clip else ([grads[k] for k in names], 0.0)
+        grads = dict(zip(names, clipped))
+        norms.append(norm)
+        losses.append(ls)
+        for k in params:
+            enc = k.split(".")[0] in ("enc", "dec")
+            base = a.get("lr_encdec", 2e-5) if enc else a.get("lr_body", 1e-4)
+            if a.get("total_steps", 0) > 0:
+                lr = ot.lr_at(step - 1, a["total_steps"], a["warmup_steps"], base=base, warm_start=a.get("warm_start", 1e-6),
+                              final=a.get("final_lr_body", 1e-5) * base / a.get("lr_body", 1e-4))
+            else:
+                lr = base
+            ot.adam_step(params[k], grads[k], mom[k], vel[k], step, lr)
+    return losses, params, p0, norms
+
+
+def _assert_updates(oc, d, params, p0, tol=1e-3):
+    from oracle import model as om
+    R, C, rr, cc = d["rc"]
+    upd_got = np.concatenate([(d["params"][k] - om.local_tile(oc, k, p0[k], R, C, rr, cc)).ravel() for k in params])
+    upd_ref = np.concatenate([(om.local_tile(oc, k, params[k] - p0[k], R, C, rr, cc)).ravel() for k in params])
+    assert np.linalg.norm(upd_got - upd_ref) / np.linalg.norm(upd_ref) < tol
+
+
+def _oc():
+    from oracle import model as om
+    meta = json.load(open(os.path.join(GOLD, "comm_golden.json")))
+    return om.Config(**{**meta["config"], "grid": tuple(meta["config"]["grid"]), "patch": tuple(meta["config"]["patch"])})
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_train_step_schedule_and_global_clip_match_oracle(world):
+    """lr_at warm-up + cosine (device schedule) and global-norm clipping over the sharded set
+    (duplicated vectors counted once) reproduce the serial oracle, tile by tile."""
+    from oracle import model as om, train as ot
+    oc = _oc()
+    z = np.load(os.path.join(GOLD, "wm_golden.npz"))
+    model = om.SerialModel(oc, om.init_params(oc, 0, np.float64))
+    _, g = ot.weighted_mse_loss(model.forward(z["x"][:1]), z["g_out"][:1] * 0.5, ot.lat_weights(oc.grid[0]),
+                                np.ones(oc.n_vars))
+    grads = model.backward(g)
+    clip = 0.5 * float(np.sqrt(sum(float((v * v).sum()) for v in grads.values())))  # clipping active
+    adam = {"warmup_steps": 1, "total_steps": 4}
+    losses, params, p0, norms = _oracle_train(oc, [0], 3, adam, clip)
+    assert norms[0] > clip
+    res = _run(world, mode="train", opts={"adam": {**adam, "clip_norm": clip}, "steps": 3})
+    want_scale = [min(1.0, clip / nm) for nm in norms]
+    want_lr = [[ot.lr_at(s, 4, 1, base=b, final=1e-5 * b / 1e-4) for b in (2e-5, 1e-4)] for s in range(3)]
+    assert want_lr[0] == [1e-6, 1e-6] and want_lr[1] == [2e-5, 1e-4]
+    for d in res:
+        assert np.allclose(d["losses"], [ls[0] for ls in losses], rtol=1e-5), (d["losses"], losses)
+        assert np.allclose(d["scales"], want_scale, rtol=1e-5), (d["scales"], want_scale)
+        assert np.allclose(d["lrs"], want_lr, rtol=1e-6), (d["lrs"], want_lr)
+        _assert_updates(oc, d, params, p0)
+
+
+@pytest.mark.parametrize("world,n_mp", [(2, 1), (4, 2)])
+def test_dp_replicas_match_serial_batch(world, n_mp):
+    """DP-equivalence: replicas of an n_mp-way model on different samples,
+    gradients averaged over the r % n groups, equal a serial run on the mean gradient; shards
+    stay identical across replicas."""
+    oc = _oc()
+    reps = world // n_mp
+    losses, params, p0, _ = _oracle_train(oc, list(range(reps)), 2)
+    res = _run(world, mode="train", opts={"mp": n_mp, "dp": True, "steps": 2})
+    for d in res:
+        k = d["rank"] // n_mp
+        assert np.allclose(d["losses"], [ls[k] for ls in losses], rtol=1e-5), (d["losses"], losses)
+        _assert_updates(oc, d, params, p0)
+    by_pos = {}
+    for d in res:
+        by_pos.setdefault(d["pos"], []).append(d)
+    for pos, ds in by_pos.items():
+        for k in ds[0]["params"]:
+            assert np.array_equal(ds[0]["params"][k], ds[-1]["params"][k]), (pos, k)
+
+
+def test_train_step_symmetric_memory_8way():
+    """Full step (loss, backward, grad sync, clip, scheduled Adam) on the 4 x 2 grid through the
+    peer-memory transport plumbing."""
+    from oracle import model as om, train as ot
+    oc = _oc()
+    z = np.load(os.path.join(GOLD, "wm_golden.npz"))
+    model = om.SerialModel(oc, om.init_params(oc, 0, np.float64))
+    _, g = ot.weighted_mse_loss(model.forward(z["x"][:1]), z["g_out"][:1] * 0.5, ot.lat_weights(oc.grid[0]),
+                                np.ones(oc.n_vars))
+    clip = 0.5 * float(np.sqrt(sum(float((v * v).sum()) for v in model.backward(g).values())))
+    adam = {"warmup_steps": 1, "total_steps": 4}
+    losses, params, p0, norms = _oracle_train(oc, [0], 2, adam, clip)
+    res = _run(8, mode="train", opts={"adam": {**adam, "clip_norm": clip}, "steps": 2, "transport": "shm"})
+    for d in res:
+        assert np.allclose(d["losses"], [ls[0] for ls in losses], rtol=1e-5), (d["losses"], losses)
+        assert np.allclose(d["scales"], [min(1.0, clip / nm) for nm in norms], rtol=1e-5)
+        _assert_updates(oc, d, params, p0)
