@@ -55,6 +55,25 @@ def parse():
     return ap.parse_args()
 
 
+def profiled_traffic(config, world):
+    """DRAM bytes per GEMM launch (dram__bytes_read.sum + dram__bytes_write.sum) from the newest
+    committed ncu summary of this bench command (profiles/*_gemm_traffic.json, written by
+    tools/ncu_summary.py); None when there is none for this configuration."""
+    if config != "C4" or world != 1:
+        return None, None
+    import glob
+    here = os.path.dirname(os.path.abspath(__file__))
+    files = sorted(glob.glob(os.path.join(here, "profiles", "*_gemm_traffic.json")))  # tags sort by round
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        if d.get("traffic_bytes_per_launch"):
+            return d["traffic_bytes_per_launch"], "profiles/" + os.path.basename(f)
+    return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -246,8 +265,10 @@ def run_ours(args, rank, world):
     s1.record(stream)
     torch.cuda.synchronize()
     recs, T.GEMM_TIMER = T.GEMM_TIMER, None
-    gemm_ms = sum(a.elapsed_time(b) for a, b, _ in recs)
-    gemm_flops = sum(f for _, _, f in recs)
+    gemm_ms = sum(a.elapsed_time(b) for a, b, _, _ in recs)
+    gemm_flops = sum(f for _, _, f, _ in recs)
+    gemm_bytes = sum(nb for _, _, _, nb in recs)
+    traffic, traffic_src = profiled_traffic(args.config, world)
     eager_ms = s0.elapsed_time(s1)
 
     burst, sustained, hbm, peak_kind = peaks()
@@ -271,7 +292,9 @@ def run_ours(args, rank, world):
             "pct_bf16_peak_basis": f"sustained {sustained} TFLOP/s per GPU ({peak_kind})",
             "roofline": {"bound": "tensor", "kernel": "jg_gemm (tcgen05, all GEMM launches of one step)",
                          "achieved": achieved, "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
-                         "traffic": None, "launches": len(recs), "gemm_share_of_eager_step": gemm_ms / eager_ms,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": gemm_bytes / max(1, len(recs)),
+                         "launches": len(recs), "gemm_share_of_eager_step": gemm_ms / eager_ms,
                          "peak_basis": f"{peak_kind} sustained bf16 (kernel timed inside a long step)"},
             "clocks": clock,
             "e2e": {"value": args.batch / (e2e_ms / 1e3), "unit": "samples/s",

@@ -12,6 +12,7 @@ and 482-490 (see train.py).
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -23,7 +24,8 @@ from .train import AdamConfig
 
 class TrainStep:
     def __init__(self, model: WeatherMixerModel, batch: int = 1, r: int = 1, adam: AdamConfig | None = None,
-                 graph: bool = True, loss_scale: float = 1.0, fused_adam: bool = False):
+                 graph: bool = True, loss_scale: float = 1.0, fused_adam: bool = False,
+                 step_count: torch.Tensor | None = None):
         self.model, self.batch, self.r = model, batch, r
         # Every weight receives exactly one gradient GEMM per step at rollout 1 (one per sample
         # on the grid path): the GEMM overwrites the fp32 gradient (no zeroing, no read-back) and
@@ -43,7 +45,8 @@ class TrainStep:
         self.ws = model.workspace(batch, r)
         dev = model.device
         self.target = torch.zeros_like(self.ws.xin)
-        self.step_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        # Adam step counter (device; shared by the per-rollout steps of one Trainer)
+        self.step_count = step_count if step_count is not None else torch.zeros(1, dtype=torch.int32, device=dev)
         self.lr_dev = torch.zeros(_lib.JG_MAX_LR_CLASSES, dtype=torch.float32, device=dev)  # this step's lr per class
         self.grad_scale = torch.ones(1, dtype=torch.float32, device=dev)                # clip factor
         self.sqsum = torch.zeros(1, dtype=torch.float32, device=dev)                    # global squared grad norm
@@ -180,9 +183,13 @@ class TrainStep:
             self.ws.xin.copy_(x)
             self.target.copy_(target)
         loss = self.run_device(ev)
-        self._pinned_loss.copy_(loss, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        self._pinned_loss.copy_(loss, non_blocking=cur is not None)
+        if cur is not None:
+            cur.synchronize()
         return float(self._pinned_loss.item())
+
+    def sync_loss(self) -> float:
+        return float(self.ws.loss.item())
 
     @property
     def h2d_bytes_per_step(self) -> int:
@@ -191,3 +198,48 @@ class TrainStep:
     @property
     def d2h_bytes_per_step(self) -> int:
         return self._d2h_bytes
+
+
+class Trainer:
+    """train_epoch / finetune_rollout: per step load this
+    rank's tile (data.TileLoader, read ahead on a host thread), run the captured step (forward
+    with rollout r, loss vs the target at lead r, backward, grad sync, dp_reduce, clip, scheduled
+    Adam). Fine-tuning draws r ~ Uniform{1..r_max} from default_rng(seed), the same sequence on
+    every rank; one CUDA graph per r, all sharing one Adam step counter."""
+
+    def __init__(self, model: WeatherMixerModel, batch: int = 1, adam: AdamConfig | None = None, r_max: int = 1,
+                 seed: int = 0, graph: bool = True):
+        self.model, self.batch, self.adam, self.r_max, self.graph = model, batch, adam or AdamConfig(), r_max, graph
+        self.rng = np.random.default_rng(seed)
+        self.step_count = torch.zeros(1, dtype=torch.int32, device=model.device)
+        self.steps: dict[int, TrainStep] = {}
+
+    def step_for(self, r: int) -> TrainStep:
+        if r not in self.steps:
+            self.steps[r] = TrainStep(self.model, self.batch, r, self.adam, graph=self.graph,
+                                      step_count=self.step_count)
+        return self.steps[r]
+
+    def draw_rollouts(self, n: int) -> np.ndarray:
+        if self.r_max == 1:
+            return np.ones(n, dtype=np.int64)
+        return self.rng.integers(1, self.r_max + 1, size=n)
+
+    def train_epoch(self, loader, epoch: int = 0, max_steps: int | None = None) -> dict:
+        """One pass over this replica's share of the samples; returns mean loss, per-step losses
+        and rollouts, and the wall time."""
+        import time
+        nb = loader.steps_per_epoch() if max_steps is None else min(max_steps, loader.steps_per_epoch())
+        rs = self.draw_rollouts(nb)
+        if self.r_max > 1 and loader.lead < self.r_max:
+            raise ConfigError(f"loader lead {loader.lead} < r_max {self.r_max}: build it with lead=r_max")
+        losses = []
+        t0 = time.perf_counter()
+        for s, (x, t) in enumerate(loader.epoch(epoch, leads=rs if self.r_max > 1 else None)):
+            if s >= nb:
+                break
+            losses.append(self.step_for(int(rs[s]))(x, t))
+        return {"loss": float(np.mean(losses)) if losses else float("nan"), "losses": losses,
+                "rollouts": rs[:len(losses)].tolist(), "seconds": time.perf_counter() - t0}
+
+    finetune_rollout = train_epoch

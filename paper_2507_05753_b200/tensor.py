@@ -26,7 +26,8 @@ from .errors import ShapeError
 DTYPES = {"f32": torch.float32, "bf16": torch.bfloat16}
 
 # Optional per-launch GEMM timer (bench.py roofline leg): a list collecting
-# (start_event, end_event, algorithmic_flops) for every jg_gemm launch while set.
+# (start_event, end_event, algorithmic_flops, algorithmic_bytes) for every jg_gemm launch while
+# set; bytes = operands read once + output written once (+ read when accumulating).
 GEMM_TIMER: list | None = None
 
 
@@ -136,7 +137,10 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
         s.record()
         _lib.gemm_raw(d)
         e.record()
-        GEMM_TIMER.append((s, e, 2 * m * n * k * batch))
+        ae, oe = a.element_size(), out.element_size()
+        outs = 1 if reduce_batch else batch
+        nbytes = (m * k + n * k) * ae * batch + m * n * oe * outs * (2 if epi & _lib.EPI_ACCUM else 1)
+        GEMM_TIMER.append((s, e, 2 * m * n * k * batch, nbytes))
     else:
         _lib.gemm_raw(d)
     return out

@@ -200,3 +200,36 @@ def test_dp_groups_rule():
     assert ProcessGroup.dp_groups(8, 2) == [[0, 2, 4, 6], [1, 3, 5, 7]]
     assert ProcessGroup.dp_groups(8, 4) == [[0, 4], [1, 5], [2, 6], [3, 7]]
     assert ProcessGroup(4, 4, 1).dp_replicas == 1
+
+
+def test_tile_loader_reads_rank_tiles_with_padding(tmp_path):
+    """each rank reads exactly oracle.local_sample of the zero-padded sample (and of
+    sample + lead as the target); mp-group members share the order, dp replicas split it."""
+    from types import SimpleNamespace
+    from paper_2507_05753_b200.data import TileLoader
+    cfg = ModelConfig(n_vars=8, grid=(32, 64), patch=(4, 4), d_emb=64, d_tok=128, d_ch=64, n_blocks=1)
+    oc = om.Config(n_vars=8, grid=(32, 64), patch=(4, 4), d_emb=64, d_tok=128, d_ch=64, n_blocks=1)
+    rng = np.random.default_rng(3)
+    src = rng.standard_normal((9, 30, 64, 7)).astype(np.float32)  # 30 real rows, 7 real vars
+    np.save(tmp_path / "era.npy", src)
+    padded = np.zeros((9, 32, 64, 8), np.float32)
+    padded[:, :30, :, :7] = src
+    for (R, C) in ((1, 1), (1, 2), (2, 2), (4, 2)):
+        for r in range(R):
+            for c in range(C):
+                ctx = SimpleNamespace(R=R, C=C, r=r, c=c, dp_index=0, dp_replicas=1)
+                ld = TileLoader(str(tmp_path / "era.npy"), cfg, ctx, lead=2, batch=2, seed=5, pin=False)
+                order = ld.order(0)
+                got = [(x.clone(), t.clone()) for x, t in ld.epoch(0)]
+                assert len(got) == ld.steps_per_epoch() == 3
+                for s, (x, t) in enumerate(got):
+                    ids = order[2 * s:2 * s + 2]
+                    assert np.array_equal(x.numpy(), om.local_sample(oc, padded[ids], R, C, r, c))
+                    assert np.array_equal(t.numpy(), om.local_sample(oc, padded[ids + 2], R, C, r, c))
+    base = TileLoader(src, cfg, SimpleNamespace(R=1, C=2, r=0, c=1, dp_index=0, dp_replicas=1), pin=False).order(1)
+    shares = [TileLoader(src, cfg, SimpleNamespace(R=1, C=2, r=0, c=0, dp_index=k, dp_replicas=2), pin=False).order(1)
+              for k in range(2)]
+    assert len(shares[0]) == len(shares[1]) and not set(shares[0]) & set(shares[1])
+    assert set(shares[0]) | set(shares[1]) <= set(base)
+    with pytest.raises(ConfigError):
+        TileLoader(src[:, :, :32], cfg, SimpleNamespace(R=1, C=1, r=0, c=0), pin=False)

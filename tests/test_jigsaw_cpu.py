@@ -57,6 +57,65 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
         g = z["g_out"][:1] if r > 1 else z["g_out"]
         xl = om.local_sample(oc, x, ctx.R, ctx.C, ctx.r, ctx.c)
         gl = om.local_sample(oc, g, ctx.R, ctx.C, ctx.r, ctx.c)
+        if mode == "trainer":
+            from paper_2507_05753_b200.data import TileLoader
+            from paper_2507_05753_b200.engine import Trainer
+            src = np.random.default_rng(7).standard_normal((6, *oc.grid, oc.n_vars)).astype(np.float32)
+            ld = TileLoader(src, cfg, ctx, lead=2, batch=1, seed=3)
+            tr = Trainer(model, batch=1, r_max=2, seed=11, graph=False)
+            st = tr.train_epoch(ld, 0, max_steps=3)
+            out_q.put({"pos": ctx.pos, "rank": rank, "rc": (ctx.R, ctx.C, ctx.r, ctx.c), "losses": st["losses"],
+                       "rollouts": st["rollouts"], "order": ld.order(0).tolist(),
+                       "params": {k_: p.data.numpy().copy() for k_, p in model.params.items()}})
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+                dist.destroy_process_group()
+            return
+        if mode in ("ckpt", "ckpt_load"):
+            from paper_2507_05753_b200 import checkpoint as ck
+            from paper_2507_05753_b200.engine import TrainStep
+            from paper_2507_05753_b200.errors import ConfigError
+            tl = om.local_sample(oc, z["g_out"][:1] * 0.5, ctx.R, ctx.C, ctx.r, ctx.c)
+            d0 = opts["dir"]
+
+            def run(st, k):
+                ls = []
+                for _ in range(k):
+                    st.ws.xin.copy_(torch.tensor(xl[:1], dtype=torch.float32))
+                    st.target.copy_(torch.tensor(tl, dtype=torch.float32))
+                    st._body()
+                    ls.append(float(st.ws.loss.item()))
+                return ls
+            if mode == "ckpt_load":
+                st = TrainStep(model, batch=1, graph=False)
+                try:
+                    ck.load(st, d0)
+                    err = None
+                except ConfigError as e:
+                    err = str(e)
+                out_q.put({"pos": ctx.pos, "rank": rank, "err": err})
+            else:
+                st = TrainStep(model, batch=1, graph=False)
+                run(st, 2)
+                ck.save(st, os.path.join(d0, "a"))
+                cont = run(st, 1)
+                p_cont = {k_: p.data.numpy().copy() for k_, p in model.params.items()}
+                model2 = WeatherMixerModel(ctx, cfg, seed=1, dtype="f32", device="cpu")  # different init
+                st2 = TrainStep(model2, batch=1, graph=False)
+                hdr = ck.load(st2, os.path.join(d0, "a"))
+                ck.save(st2, os.path.join(d0, "b"))
+                f = ck.shard_path("", ctx.pos, ctx.n)
+                same = open(os.path.join(d0, "a", f), "rb").read() == open(os.path.join(d0, "b", f), "rb").read()
+                resumed = run(st2, 1)
+                p_res = {k_: p.data.numpy().copy() for k_, p in model2.params.items()}
+                out_q.put({"pos": ctx.pos, "rank": rank, "same": same, "cont": cont, "resumed": resumed,
+                           "step": hdr["step"], "params_equal": all(np.array_equal(p_cont[k_], p_res[k_]) for k_ in p_cont)})
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+                dist.destroy_process_group()
+            return
         if mode == "train":
             from paper_2507_05753_b200.engine import TrainStep
             from paper_2507_05753_b200.train import AdamConfig
@@ -305,4 +364,53 @@ def test_train_step_symmetric_memory_8way():
     for d in res:
         assert np.allclose(d["losses"], [ls[0] for ls in losses], rtol=1e-5), (d["losses"], losses)
         assert np.allclose(d["scales"], [min(1.0, clip / nm) for nm in norms], rtol=1e-5)
+        _assert_updates(oc, d, params, p0)
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_checkpoint_roundtrip_and_resume(world, tmp_path):
+    """save -> load -> save is byte-identical; a resumed run reproduces the
+    uninterrupted run's next step exactly; one file per rank."""
+    res = _run(world, mode="ckpt", opts={"dir": str(tmp_path)})
+    assert len(os.listdir(tmp_path / "a")) == world
+    for d in res:
+        assert d["same"] and d["step"] == 2
+        assert d["cont"] == d["resumed"] and d["params_equal"]
+
+
+def test_checkpoint_world_shape_mismatch(tmp_path):
+    """Loading a 4-way checkpoint into a 2-way world is an explicit error naming both shapes."""
+    _run(4, mode="ckpt", opts={"dir": str(tmp_path)})
+    res = _run(2, mode="ckpt_load", opts={"dir": str(tmp_path / "a")})
+    for d in res:
+        assert d["err"] is not None and "4-way" in d["err"] and "2-way" in d["err"], d["err"]
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_trainer_rollout_finetune_matches_oracle(world):
+    """finetune_rollout: tiles from the loader, r ~ U{1, 2} from a seeded generator (same on every
+    rank), loss vs the target at lead r, one Adam counter across the per-r steps — equal to the
+    serial oracle fed the same samples."""
+    from oracle import model as om, train as ot
+    oc = _oc()
+    res = _run(world, mode="trainer")
+    src = np.random.default_rng(7).standard_normal((6, *oc.grid, oc.n_vars))
+    rs, order = res[0]["rollouts"], res[0]["order"]
+    assert all(d["rollouts"] == rs and d["order"] == order for d in res) and set(rs) <= {1, 2}
+    params = om.init_params(oc, 0, np.float64)
+    p0 = {k: v.copy() for k, v in params.items()}
+    mom = {k: np.zeros_like(v) for k, v in params.items()}
+    vel = {k: np.zeros_like(v) for k, v in params.items()}
+    losses = []
+    for s, r in enumerate(rs):
+        i = order[s]
+        model = om.SerialModel(oc, params)
+        loss, g = ot.weighted_mse_loss(model.forward(src[i:i + 1], r=r), src[i + r:i + r + 1],
+                                       ot.lat_weights(oc.grid[0]), np.ones(oc.n_vars))
+        grads = model.backward(g)
+        losses.append(loss)
+        for k in params:
+            ot.adam_step(params[k], grads[k], mom[k], vel[k], s + 1, 2e-5 if k.split(".")[0] in ("enc", "dec") else 1e-4)
+    for d in res:
+        assert np.allclose(d["losses"], losses, rtol=1e-5), (d["losses"], losses)
         _assert_updates(oc, d, params, p0)
