@@ -51,6 +51,7 @@ class TrainStep:
         self.grad_scale = torch.ones(1, dtype=torch.float32, device=dev)                # clip factor
         self.sqsum = torch.zeros(1, dtype=torch.float32, device=dev)                    # global squared grad norm
         self.use_graph = graph
+        self._dry = False
         self.graph = None
         self.launches_per_step = None
         self._pinned_loss = torch.zeros(1, dtype=torch.float32, pin_memory=dev.type == "cuda")
@@ -65,7 +66,8 @@ class TrainStep:
     def _body_fwd(self) -> None:
         """Step counter, gradient zeroing, forward (needs only x)."""
         m, ws, f = self.model, self.ws, self.model.flat
-        K.step_increment(self.step_count)
+        if not self._dry:
+            K.step_increment(self.step_count)
         if self.fused_adam or self.overwrite:
             for cls in f.CLASSES:  # matrix gradients are written whole by their GEMM; vectors accumulate
                 lo, hi = f.vec_range(cls)
@@ -81,7 +83,7 @@ class TrainStep:
         m._blend(ws, target=self.target, loss=ws.loss, loss_scale=self.loss_scale)
         if m.ctx.n > 1:
             m.ctx.all_reduce_all(ws.loss)  # the loss is a sum of per-tile terms
-        m._fused_adam = (self.step_count, self.adam) if self.fused_adam else None
+        m._fused_adam = (self.step_count, self.adam) if self.fused_adam and not self._dry else None
         m._grad_overwrite = self.overwrite
         try:
             m._backward(ws)
@@ -90,6 +92,8 @@ class TrainStep:
             m._grad_overwrite = False
         m.grad_sync()
         m.ctx.all_reduce_dp_mean(m.flat.grad)  # dp_reduce over replicas of this shard (no-op for one)
+        if self._dry:
+            return
         if self.clip is not None:
             self._global_sqnorm()
         if self.clip is not None or self.scheduled:
@@ -124,23 +128,28 @@ class TrainStep:
                    lr_dev=self.lr_dev[i:i + 1] if self.scheduled else None)
 
     def capture(self) -> None:
-        """Warm up on a side stream, then capture the step into two CUDA graphs (forward | loss +
-        backward + Adam) sharing one memory pool, so the public call can overlap the target's
-        host->device copy with the forward."""
+        """Warm up on a side stream with a dry step (forward, loss, backward, gradient sync: no
+        optimiser update, no step count — lazy initialisation of communicators and kernels
+        happens outside the capture and the training state is untouched), then capture the step
+        into two CUDA graphs (forward | loss + backward + Adam) sharing one memory pool, so the
+        public call can overlap the target's host->device copy with the forward."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            before = _lib.launch_count()
-            self._body()
-            self.launches_per_step = _lib.launch_count() - before
+            self._dry = True
+            try:
+                self._body()
+            finally:
+                self._dry = False
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        # the warm-up was a real training step (Adam state and step counter advanced)
+        before = _lib.launch_count()
         g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(g1):
             self._body_fwd()
         with torch.cuda.graph(g2, pool=g1.pool()):
             self._body_bwd()
+        self.launches_per_step = _lib.launch_count() - before
         self.graph = (g1, g2)
         torch.cuda.synchronize()
 
