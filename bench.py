@@ -178,6 +178,20 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def fill_random_inputs(step, lat_real, seed):
+    """Synthetic z-scored inputs in the step's resident buffers: x, target ~ N(0, 1), padded rows
+    zero (random data matters: the GEMMs are power-capped and zero operands draw less power)."""
+    import torch
+    g = torch.Generator(device=step.ws.xin.device).manual_seed(seed)
+    xd = torch.randn(step.ws.xin.shape, device=step.ws.xin.device, generator=g)
+    td = torch.randn(step.ws.xin.shape, device=step.ws.xin.device, generator=g)
+    xd[:, lat_real:] = 0
+    td[:, lat_real:] = 0
+    step.ws.xin.copy_(xd)
+    step.target.copy_(td)
+    return xd, td
+
+
 def run_ours(args, rank, world):
     import numpy as np
     import torch
@@ -200,13 +214,7 @@ def run_ours(args, rank, world):
     # synthetic z-scored inputs: x, target ~ N(0, 1); padded rows / channels are zero
     lat, lon = model.local_grid
     nv = model.local_vars
-    g = torch.Generator(device="cuda").manual_seed(1234 + ctx.pos)
-    xd = torch.randn((args.batch, lat, lon, nv), device="cuda", generator=g)
-    td = torch.randn((args.batch, lat, lon, nv), device="cuda", generator=g)
-    xd[:, lat_real:] = 0
-    td[:, lat_real:] = 0
-    step.ws.xin.copy_(xd)
-    step.target.copy_(td)
+    xd, td = fill_random_inputs(step, lat_real, 1234 + ctx.pos)
 
     def barrier():
         if world > 1:

@@ -29,6 +29,16 @@ __device__ __forceinline__ void store1_bc(void* base, const Bcast& bc, int64_t o
   for (int i = 0; i < bc.n; ++i) jgd::store1(bc.p[i], off, bf16, v);
 }
 
+// Grid of at most (resident blocks per SM) x (SM count) for a grid-stride kernel: every block
+// is resident from the start, so there is no second partial wave.
+template <typename Kern>
+int resident_grid(Kern kernel, int block, int64_t work_blocks) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  const int64_t cap = static_cast<int64_t>(per_sm) * jg::num_sms();
+  return static_cast<int>(work_blocks < 1 ? 1 : (work_blocks < cap ? work_blocks : cap));
+}
+
 int grid_for(int64_t work_items, int per_block) {
   int64_t b = (work_items + per_block - 1) / per_block;
   const int64_t cap = static_cast<int64_t>(jg::num_sms()) * 16;
@@ -314,28 +324,90 @@ __global__ void rowsum_kernel(const void* __restrict__ x, bool bf16, float* __re
 
 // ---------------------------------------------------------------- patch permutes
 // token t = gi*gw + gj ; feature f = c*pl*pw + i*pw + j ; grid (gi*pl+i, gj*pw+j, c)
-// One CTA per patch (grid-stride over tokens): the patch's p_lat rows of p_lon*C contiguous
-// grid values are read coalesced into smem laid out [C][p_lat*p_lon + 1] (the +1 pad makes
-// the channel-strided accesses bank-conflict free), then written as one contiguous token row.
+// Work unit = (b, gi, i, gj, c), c fastest: the pw grid values of channel c along one patch
+// row (lanes = consecutive channels, so each of the pw loads is a coalesced warp-wide run) map
+// to pw CONTIGUOUS token features c*pl*pw + i*pw + [0, pw) — one 8/16/32-byte vector per
+// thread (whole 32-byte sectors; the neighbouring rows' halves merge in L2). Every unit is
+// independent: no shared-memory transpose, no barriers, pw loads in flight per thread.
+struct PatchIdx {
+  int64_t b, y, gj, tk;
+  int c, i;
+};
+__device__ __forceinline__ PatchIdx patch_unit(uint32_t u, int chans, uint32_t gw, int pl, uint32_t gh) {
+  PatchIdx q;
+  q.c = static_cast<int>(u % chans);
+  u /= chans;
+  q.gj = u % gw;
+  u /= gw;
+  q.i = static_cast<int>(u % pl);
+  u /= pl;
+  const int64_t gi = u % gh;
+  q.b = u / gh;
+  q.y = gi * pl + q.i;
+  q.tk = (q.b * gh + gi) * gw + q.gj;
+  return q;
+}
+
+template <int PW>
+__device__ __forceinline__ void store_run(void* base, int64_t off, bool bf16, const float* v) {
+  if constexpr (PW == 8) {
+    jgd::store8(base, off, bf16, v);
+  } else if constexpr (PW == 4) {
+    if (bf16) {
+      uint2 raw;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+      h[0] = __floats2bfloat162_rn(v[0], v[1]);
+      h[1] = __floats2bfloat162_rn(v[2], v[3]);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + off) = raw;
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  } else if constexpr (PW == 2) {
+    if (bf16)
+      *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(base) + off) = __floats2bfloat162_rn(v[0], v[1]);
+    else
+      *reinterpret_cast<float2*>(reinterpret_cast<float*>(base) + off) = make_float2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < PW; ++j) jgd::store1(base, off + j, bf16, v[j]);
+  }
+}
+template <int PW>
+__device__ __forceinline__ void load_run(const float* base, int64_t off, float* v) {
+  if constexpr (PW == 8) {
+    jgd::load8(base, off, false, v);
+  } else if constexpr (PW == 4) {
+    const float4 a = *reinterpret_cast<const float4*>(base + off);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  } else if constexpr (PW == 2) {
+    const float2 a = *reinterpret_cast<const float2*>(base + off);
+    v[0] = a.x; v[1] = a.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < PW; ++j) v[j] = base[off + j];
+  }
+}
+
+// PW > 0: compile-time patch width (vector path); PW == 0: runtime width, scalar token side.
+template <int PW>
 __global__ void patchify_kernel(const float* __restrict__ x, void* __restrict__ tok, bool bf16, int64_t batch,
-                                int64_t lat, int64_t lon, int64_t chans, int64_t pl, int64_t pw) {
-  extern __shared__ float sm[];
-  const int64_t gw = lon / pw, T = (lat / pl) * gw;
-  const int C = static_cast<int>(chans), PL = static_cast<int>(pl), PW = static_cast<int>(pw);
-  const int PP = PL * PW, PS = PP + 1, F = C * PP, RW = PW * C;  // RW: contiguous run per patch row
-  for (int64_t tk = blockIdx.x; tk < batch * T; tk += gridDim.x) {
-    const int64_t b = tk / T, t = tk % T, gi = t / gw, gj = t % gw;
-    const float* src = x + ((b * lat + gi * pl) * lon + gj * pw) * chans;
-    for (int e = threadIdx.x; e < F; e += blockDim.x) {
-      const int i = e / RW, r = e - i * RW, j = r / C, c = r - j * C;
-      sm[c * PS + i * PW + j] = src[static_cast<int64_t>(i) * lon * chans + r];
+                                int64_t lat, int64_t lon, int chans, int pl, int pw_rt) {
+  const int pw = PW > 0 ? PW : pw_rt;
+  const uint32_t gw = static_cast<uint32_t>(lon / pw), gh = static_cast<uint32_t>(lat / pl);
+  const uint32_t units = static_cast<uint32_t>(batch) * gh * pl * gw * chans;
+  const int64_t PP = static_cast<int64_t>(pl) * pw, F = PP * chans;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < units; u += gridDim.x * blockDim.x) {
+    const PatchIdx q = patch_unit(u, chans, gw, pl, gh);
+    const float* src = x + ((q.b * lat + q.y) * lon + q.gj * pw) * chans + q.c;
+    const int64_t dst = q.tk * F + q.c * PP + q.i * pw;
+    if constexpr (PW > 0) {
+      float v[PW];
+#pragma unroll
+      for (int j = 0; j < PW; ++j) v[j] = src[static_cast<int64_t>(j) * chans];
+      store_run<PW>(tok, dst, bf16, v);
+    } else {
+      for (int j = 0; j < pw; ++j) jgd::store1(tok, dst + j, bf16, src[static_cast<int64_t>(j) * chans]);
     }
-    __syncthreads();
-    for (int f = threadIdx.x; f < F; f += blockDim.x) {
-      const int c = f / PP, rr = f - c * PP;
-      jgd::store1(tok, tk * F + f, bf16, sm[c * PS + rr]);
-    }
-    __syncthreads();
   }
 }
 
@@ -355,80 +427,96 @@ __global__ void unpatchify_kernel(const float* __restrict__ tok, float* __restri
 }
 
 // ---------------------------------------------------------------- blend + loss
-// One CTA per patch (grid-stride): the decoder token row is read contiguously into smem
-// [C][p_lat*p_lon + 1]; x / target / out are touched in grid order (coalesced runs of
-// p_lon*C); the gradient token row is staged in smem and written contiguously. Per-channel
-// blend gradients and the loss accumulate in smem; one atomic per channel per CTA.
-constexpr int MAX_CH = 1024;
-// Threads t < C * floor(blockDim / C) each own channel t % C for the whole kernel: the grid
-// element loop strides by a multiple of C, so blend-gradient and loss partials stay in registers.
+// Same work units as patchify (b, gi, i, gj, c): one vector of pw decoder features per thread,
+// pw coalesced x / target (/ out / g_ext) values, one vector of pw gradient features stored.
+// The grid-stride step is a multiple of C (only the first C*floor(blockDim/C) threads of a
+// block work), so each thread keeps ONE channel for the whole kernel and its blend-gradient
+// and loss partials stay in registers; one shared atomic per thread and one global atomic per
+// channel per block at the end.
+constexpr int MAX_CH = 256;
+template <int PW>
 __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float* __restrict__ x,
                                   const float* __restrict__ target, const float* __restrict__ blend_w,
                                   const float* __restrict__ lat_w, const float* __restrict__ var_w,
                                   const float* __restrict__ g_ext, float* __restrict__ out, float* __restrict__ loss_sum,
                                   float* __restrict__ g_blend, float* __restrict__ g_dec_f32,
                                   __nv_bfloat16* __restrict__ g_dec_bf16, int64_t batch, int64_t lat, int64_t lon,
-                                  int64_t chans, int64_t pl, int64_t pw, float inv_count, float loss_scale,
-                                  const Bcast bc) {
-  extern __shared__ float sm[];
+                                  int chans, int pl, int pw_rt, float inv_count, float loss_scale, const Bcast bc) {
   __shared__ float s_gb[MAX_CH];
   __shared__ float s_loss[32];
-  const int64_t gw = lon / pw, T = (lat / pl) * gw;
-  const int C = static_cast<int>(chans), PL = static_cast<int>(pl), PW = static_cast<int>(pw);
-  const int PP = PL * PW, PS = PP + 1, F = C * PP, RW = PW * C;
-  float* sdec = sm;          // [C][PS]
-  float* sgd = sm + C * PS;  // [C][PS]
+  const int pw = PW > 0 ? PW : pw_rt;
+  const int C = chans;
+  const uint32_t gw = static_cast<uint32_t>(lon / pw), gh = static_cast<uint32_t>(lat / pl);
+  const uint32_t units = static_cast<uint32_t>(batch) * gh * pl * gw * C;
+  const int64_t PP = static_cast<int64_t>(pl) * pw, F = PP * C;
   const bool want_grad = (g_ext != nullptr) || (target != nullptr);
-  const int stride = (static_cast<int>(blockDim.x) / C) * C;  // > 0: host guarantees C <= blockDim
+  const int act = (static_cast<int>(blockDim.x) / C) * C;  // > 0: host guarantees C <= blockDim
   const int t0 = static_cast<int>(threadIdx.x);
-  const bool active = t0 < stride;
-  const int my_c = active ? t0 % C : 0;
-  const float w = blend_w[my_c], vw = var_w ? var_w[my_c] : 0.f;
   for (int c = t0; c < C; c += blockDim.x) s_gb[c] = 0.f;
+  __syncthreads();
   float lsum = 0.f, gb = 0.f;
-  for (int64_t tk = blockIdx.x; tk < batch * T; tk += gridDim.x) {
-    const int64_t b = tk / T, t = tk % T, gi = t / gw, gj = t % gw;
-    const int64_t gbase = ((b * lat + gi * pl) * lon + gj * pw) * chans;
-    __syncthreads();
-    for (int f = t0; f < F; f += blockDim.x) {
-      const int c = f / PP;
-      sdec[c * PS + (f - c * PP)] = dec_tok[tk * F + f];
-    }
-    __syncthreads();
-    if (active) {
-      for (int e = t0; e < F; e += stride) {
-        const int i = e / RW, r = e - i * RW, j = r / C;  // channel == my_c
-        const int64_t ga = gbase + static_cast<int64_t>(i) * lon * chans + r;
-        const int si = my_c * PS + i * PW + j;
-        const float dec = sdec[si];
-        const float xv = x[ga];
-        const float o = w * dec + (1.0f - w) * xv;
-        if (out) out[ga] = o;
-        if (!want_grad) continue;
-        float g;
-        if (g_ext) {
-          g = g_ext[ga];
-        } else {
-          const float wt = lat_w[gi * pl + i] * vw;
-          const float er = o - target[ga];
-          lsum += wt * er * er;
-          g = 2.0f * wt * er * inv_count * loss_scale;
+  if (t0 < act) {
+    const int my_c = t0 % C;
+    const float w = blend_w[my_c], vw = var_w ? var_w[my_c] : 0.f;
+    constexpr int VMAX = PW > 0 ? PW : 16;
+    for (uint32_t u = blockIdx.x * act + t0; u < units; u += gridDim.x * act) {
+      const PatchIdx q = patch_unit(u, C, gw, pl, gh);
+      const int64_t ga0 = ((q.b * lat + q.y) * lon + q.gj * pw) * C + my_c;
+      const int64_t to = q.tk * F + my_c * PP + q.i * pw;
+      float dec[VMAX], xv[VMAX], tv[VMAX];
+      if constexpr (PW > 0) {
+        load_run<PW>(dec_tok, to, dec);
+      } else {
+#pragma unroll
+        for (int j = 0; j < VMAX; ++j)
+          if (j < pw) dec[j] = dec_tok[to + j];
+      }
+#pragma unroll
+      for (int j = 0; j < VMAX; ++j)
+        if (PW > 0 || j < pw) {
+          xv[j] = x[ga0 + static_cast<int64_t>(j) * C];
+          tv[j] = want_grad ? (g_ext ? g_ext[ga0 + static_cast<int64_t>(j) * C] : target[ga0 + static_cast<int64_t>(j) * C])
+                            : 0.f;
         }
-        gb += g * (dec - xv);
-        sgd[si] = g * w;
+      const float wt = (target && !g_ext) ? lat_w[q.y] * vw : 0.f;
+      float gd[VMAX];
+#pragma unroll
+      for (int j = 0; j < VMAX; ++j)
+        if (PW > 0 || j < pw) {
+          const float o = w * dec[j] + (1.0f - w) * xv[j];
+          if (out) out[ga0 + static_cast<int64_t>(j) * C] = o;
+          float g;
+          if (g_ext) {
+            g = tv[j];
+          } else {
+            const float er = o - tv[j];
+            lsum += wt * er * er;
+            g = 2.0f * wt * er * inv_count * loss_scale;
+          }
+          gb += g * (dec[j] - xv[j]);
+          gd[j] = g * w;
+        }
+      if (!want_grad) continue;
+      if constexpr (PW > 0) {
+        if (g_dec_f32) {
+          store_run<PW>(g_dec_f32, to, false, gd);
+          for (int k = 0; k < bc.n; ++k) store_run<PW>(bc.p[k], to, false, gd);
+        }
+        if (g_dec_bf16) {
+          store_run<PW>(g_dec_bf16, to, true, gd);
+          for (int k = 0; k < bc.n; ++k) store_run<PW>(bc.p[k], to, true, gd);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < VMAX; ++j)
+          if (j < pw) {
+            if (g_dec_f32) store1_bc(g_dec_f32, bc, to + j, false, gd[j]);
+            if (g_dec_bf16) store1_bc(g_dec_bf16, bc, to + j, true, gd[j]);
+          }
       }
     }
-    if (!want_grad) continue;
-    __syncthreads();
-    for (int f = t0; f < F; f += blockDim.x) {
-      const int c = f / PP;
-      const float gd = sgd[c * PS + (f - c * PP)];
-      if (g_dec_f32) store1_bc(g_dec_f32, bc, tk * F + f, false, gd);
-      if (g_dec_bf16) store1_bc(g_dec_bf16, bc, tk * F + f, true, gd);
-    }
+    if (want_grad) atomicAdd(&s_gb[my_c], gb);
   }
-  __syncthreads();
-  if (active && want_grad) atomicAdd(&s_gb[my_c], gb);
   lsum = warp_sum(lsum);
   if ((threadIdx.x & 31) == 0) s_loss[threadIdx.x >> 5] = lsum;
   __syncthreads();
@@ -822,15 +910,27 @@ int jg_patchify(const float* x, void* tokens, int32_t t_type, int64_t batch, int
   JG_SHAPE_CHECK(p_lat > 0 && p_lon > 0 && lat % p_lat == 0 && lon % p_lon == 0,
                  "grid %lldx%lld not divisible by patch %lldx%lld", (long long)lat, (long long)lon, (long long)p_lat,
                  (long long)p_lon);
-  const int64_t ntok = batch * (lat / p_lat) * (lon / p_lon);
-  if (ntok == 0) return JG_OK;
-  const int64_t smem = chans * (p_lat * p_lon + 1) * 4;
-  JG_SHAPE_CHECK(smem <= 200 * 1024, "jg_patchify: patch of %lld features too large", (long long)(chans * p_lat * p_lon));
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(patchify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = static_cast<int>(ntok < jg::num_sms() * 8 ? ntok : jg::num_sms() * 8);
-  patchify_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(x, tokens, t_type == JG_BF16, batch, lat, lon, chans,
-                                                             p_lat, p_lon);
+  const int64_t units = batch * lat * (lon / p_lon) * chans;
+  if (units == 0) return JG_OK;
+  JG_SHAPE_CHECK(units < (int64_t(1) << 31), "jg_patchify: %lld patch rows exceed 2^31", (long long)units);
+  const bool bf = t_type == JG_BF16;
+  const int vb = static_cast<int>(p_lon) * (bf ? 2 : 4);  // vector bytes per thread on the token side
+  const bool al = (reinterpret_cast<uintptr_t>(tokens) % (vb >= 16 ? 16 : vb)) == 0;
+  auto* st = (cudaStream_t)stream;
+  const int C = static_cast<int>(chans), PL = static_cast<int>(p_lat), PW = static_cast<int>(p_lon);
+  const int64_t nb = (units + 255) / 256;
+#define JG_PATCH(PWV)                                                                       \
+  patchify_kernel<PWV><<<resident_grid(patchify_kernel<PWV>, 256, nb), 256, 0, st>>>(x, tokens, bf, batch, lat, \
+                                                                                      lon, C, PL, PW)
+  if (al && p_lon == 8)
+    JG_PATCH(8);
+  else if (al && p_lon == 4)
+    JG_PATCH(4);
+  else if (al && p_lon == 2)
+    JG_PATCH(2);
+  else
+    JG_PATCH(0);
+#undef JG_PATCH
   JG_LAUNCH_CHECK("patchify");
   return JG_OK;
 }
@@ -851,20 +951,40 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
                   float* g_dec_f32, void* g_dec_bf16, int64_t batch, int64_t lat, int64_t lon, int64_t chans,
                   int64_t p_lat, int64_t p_lon, float inv_count, float loss_scale, const jg_bcast* gdec_bcast,
                   void* stream) {
-  JG_SHAPE_CHECK(chans <= MAX_CH, "jg_blend_loss: at most %d channels", MAX_CH);
+  JG_SHAPE_CHECK(chans > 0 && chans <= MAX_CH, "jg_blend_loss: 1..%d channels", MAX_CH);
   JG_SHAPE_CHECK(lat % p_lat == 0 && lon % p_lon == 0, "jg_blend_loss: grid not divisible by patch");
   JG_SHAPE_CHECK(!target || (lat_w && var_w), "jg_blend_loss: a target needs lat/var weights");
-  const int64_t ntok = batch * (lat / p_lat) * (lon / p_lon);
-  if (ntok == 0) return JG_OK;
-  const int64_t smem = 2 * chans * (p_lat * p_lon + 1) * 4;
-  JG_SHAPE_CHECK(smem <= 180 * 1024, "jg_blend_loss: patch of %lld features too large", (long long)(chans * p_lat * p_lon));
-  if (smem > 40 * 1024)
-    cudaFuncSetAttribute(blend_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = static_cast<int>(ntok < jg::num_sms() * 4 ? ntok : jg::num_sms() * 4);
-  JG_SHAPE_CHECK(chans <= 256, "jg_blend_loss: at most 256 channels");
-  blend_loss_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
-      dec_tok, x, target, blend_w, lat_w, var_w, g_out_ext, out, loss_sum, g_blend, g_dec_f32,
-      (__nv_bfloat16*)g_dec_bf16, batch, lat, lon, chans, p_lat, p_lon, inv_count, loss_scale, to_bcast(gdec_bcast));
+  JG_SHAPE_CHECK(p_lon <= 16, "jg_blend_loss: patch width %lld > 16", (long long)p_lon);
+  const int64_t units = batch * lat * (lon / p_lon) * chans;
+  if (units == 0) return JG_OK;
+  JG_SHAPE_CHECK(units < (int64_t(1) << 31), "jg_blend_loss: %lld patch rows exceed 2^31", (long long)units);
+  const Bcast bc = to_bcast(gdec_bcast);
+  // vector path: every token-side base (the decoder tokens, gradient outputs, peer copies) aligned
+  // to the per-thread run (pw floats / bf16)
+  const int vf = static_cast<int>(p_lon) * 4, vh = static_cast<int>(p_lon) * 2;
+  auto al = [](const void* p, int bytes) {
+    return p == nullptr || (reinterpret_cast<uintptr_t>(p) % (bytes >= 16 ? 16 : bytes)) == 0;
+  };
+  bool vec = al(dec_tok, vf) && al(g_dec_f32, vf) && al(g_dec_bf16, vh);
+  for (int k = 0; k < bc.n; ++k) vec = vec && al(bc.p[k], g_dec_f32 ? vf : vh);
+  const int block = 256;
+  const int act = (block / static_cast<int>(chans)) * static_cast<int>(chans);
+  const int64_t nb = (units + act - 1) / act;
+  auto* st = (cudaStream_t)stream;
+  const int C = static_cast<int>(chans), PL = static_cast<int>(p_lat), PW = static_cast<int>(p_lon);
+#define JG_BLEND(PWV)                                                                                           \
+  blend_loss_kernel<PWV><<<resident_grid(blend_loss_kernel<PWV>, block, nb), block, 0, st>>>(dec_tok, x, target, blend_w, lat_w, var_w, g_out_ext, out,      \
+                                                 loss_sum, g_blend, g_dec_f32, (__nv_bfloat16*)g_dec_bf16, batch, \
+                                                 lat, lon, C, PL, PW, inv_count, loss_scale, bc)
+  if (vec && p_lon == 8)
+    JG_BLEND(8);
+  else if (vec && p_lon == 4)
+    JG_BLEND(4);
+  else if (vec && p_lon == 2)
+    JG_BLEND(2);
+  else
+    JG_BLEND(0);
+#undef JG_BLEND
   JG_LAUNCH_CHECK("blend_loss");
   return JG_OK;
 }

@@ -59,3 +59,42 @@ def test_matmul_dtype_mismatch_raises(cuda):
         T.matmul(torch.zeros(4, 4, device=cuda), torch.zeros(4, 4, device=cuda, dtype=torch.bfloat16))
     with pytest.raises(ShapeError, match="incompatible"):
         T.matmul(torch.zeros(4, 3, device=cuda), torch.zeros(4, 3, device=cuda), "NN")
+
+
+@pytest.mark.parametrize("shape,patch,gdt", [((2, 16, 32, 8), (4, 4), torch.float32), ((1, 16, 24, 70), (8, 8), torch.bfloat16),
+                                             ((1, 8, 12, 35), (2, 2), torch.bfloat16), ((1, 8, 12, 3), (2, 3), torch.float32),
+                                             ((1, 16, 16, 5), (8, 8), torch.float32)])
+def test_blend_loss_kernel(cuda, rng, shape, patch, gdt):
+    """jg_blend_loss (unpatchify + blend + lat-weighted MSE + dL/d(dec tokens) + blend-weight
+    gradient) against a float64 torch restatement of the same formulas; vector (pw 2/4/8) and
+    scalar (pw 3) token paths, fp32 and bf16 gradient tokens, target and external-gradient forms."""
+    from paper_2507_05753_b200 import kernels as K
+    from paper_2507_05753_b200 import tensor as T
+    B, lat, lon, C = shape
+    pl, pw = patch
+    f = lambda a: torch.tensor(a, dtype=torch.float32, device=cuda)  # noqa: E731
+    x, tgt = rng.standard_normal(shape), rng.standard_normal(shape)
+    dec_g = rng.standard_normal(shape)
+    w, latw, varw = rng.random(C), rng.random(lat), rng.random(C)
+    dec_tok = T.patchify(f(dec_g), pl, pw)
+    inv, ls = 1.0 / x.size, 3.0
+    # float64 restatement
+    out = w * dec_g + (1 - w) * x
+    wt = latw[None, :, None, None] * varw[None, None, None, :]
+    er = out - tgt
+    loss = (wt * er * er).sum() * inv
+    g = 2 * wt * er * inv * ls
+    gblend = (g * (dec_g - x)).sum(axis=(0, 1, 2))
+    gdec = ops.patchify((g * w).astype(np.float32), pl, pw)
+    for mode in ("target", "ext"):
+        lossd, gb = torch.zeros(1, device=cuda), torch.zeros(C, device=cuda)
+        gd = torch.zeros(dec_tok.shape, dtype=gdt, device=cuda)
+        o = torch.zeros(shape, device=cuda)
+        K.blend_loss(dec_tok, f(x), f(tgt) if mode == "target" else None, f(w), f(latw), f(varw),
+                     f(g) if mode == "ext" else None, o, lossd, gb, gd, B, lat, lon, C, pl, pw, inv, ls)
+        tol = 1e-5 if gdt == torch.float32 else 8e-3
+        assert rel_err(o.cpu().numpy(), out) < 1e-6
+        assert rel_err(gd.float().cpu().numpy(), gdec) < tol
+        assert rel_err(gb.cpu().numpy(), gblend) < 1e-4
+        if mode == "target":
+            assert abs(lossd.item() - loss) / loss < 1e-5

@@ -13,6 +13,7 @@ cfg_kw, lat_real, vars_real, _ = bench.CONFIGS[os.environ.get("CFG", "C4")]
 model = WeatherMixerModel(ctx, ModelConfig(**cfg_kw), init="fast")
 model.lat_real, model.vars_real = lat_real, vars_real
 step = TrainStep(model, graph=False)
+bench.fill_random_inputs(step, lat_real, 1234 + ctx.pos)
 recs = collections.defaultdict(list)
 
 def wrap(obj, name, label):
