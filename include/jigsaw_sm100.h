@@ -222,6 +222,24 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
 int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n,
             float lr, float beta1, float beta2, float eps, const int32_t* step_dev,
             const float* grad_scale_dev, const float* lr_dev, void* stream);   /* lr_dev != NULL overrides lr */
+/* jg_adam + Jigsaw weight-panel push: segment k of this call's range ([start, start+len),
+ * 64-element aligned, len % 4 == 0) is additionally stored as bf16 at every dst[k][0..ndst)
+ * (8-byte aligned) — the column-group members' gather slots of a channel-mixing weight, so the
+ * next step's weight-panel all-gather is done by the optimiser (replaces the per-panel copies
+ * of jigsaw_grid.gather_panels). */
+#define JG_MAX_PUSH_SEGS 16
+typedef struct jg_push_seg {
+  int64_t start, len;
+  void* dst[4];
+  int32_t ndst;
+} jg_push_seg;
+typedef struct jg_push_table {
+  jg_push_seg seg[JG_MAX_PUSH_SEGS];
+  int32_t nseg;
+} jg_push_table;
+int jg_adam_push(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n,
+                 float lr, float beta1, float beta2, float eps, const int32_t* step_dev,
+                 const float* grad_scale_dev, const float* lr_dev, const jg_push_table* push, void* stream);
 /* *counter += 1 on the device (advances the Adam step inside a graph). */
 int jg_step_increment(int32_t* counter, void* stream);
 

@@ -33,7 +33,7 @@ EXPORTED = [
     "jg_gemm", "jg_split_tf32", "jg_split_tf32_2d", "jg_cast_bf16", "jg_gelu_fwd", "jg_gelu_bwd",
     "jg_ln_moments", "jg_ln_apply", "jg_ln_bwd_moments", "jg_ln_bwd_apply",
     "jg_colsum", "jg_rowsum", "jg_patchify", "jg_unpatchify", "jg_blend_loss",
-    "jg_adam", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async",
+    "jg_adam", "jg_adam_push", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async",
     "jg_opt_schedule", "jg_version", "jg_last_error", "jg_launch_count",
 ]
 JG_MAX_LR_CLASSES = 4
@@ -54,6 +54,36 @@ def make_bcast(addrs) -> "Bcast | None":
         b.ptr[i] = a
     b.n = len(addrs)
     return b
+
+
+JG_MAX_PUSH_SEGS = 16
+
+
+class PushSeg(ctypes.Structure):
+    """jg_push_seg: a range of an Adam call whose bf16 copy is also stored at up to 4 addresses."""
+    _fields_ = [("start", ctypes.c_int64), ("len", ctypes.c_int64), ("dst", ctypes.c_void_p * 4),
+                ("ndst", ctypes.c_int32)]
+
+
+class PushTable(ctypes.Structure):
+    _fields_ = [("seg", PushSeg * JG_MAX_PUSH_SEGS), ("nseg", ctypes.c_int32)]
+
+
+def make_push_table(segs) -> "PushTable | None":
+    """segs: [(start, len, [addr, ...]), ...] relative to the Adam call's range."""
+    if not segs:
+        return None
+    if len(segs) > JG_MAX_PUSH_SEGS:
+        raise ValueError(f"at most {JG_MAX_PUSH_SEGS} push segments")
+    t = PushTable()
+    for k, (start, n, addrs) in enumerate(segs):
+        if len(addrs) > 4:
+            raise ValueError("at most 4 push destinations")
+        t.seg[k].start, t.seg[k].len, t.seg[k].ndst = start, n, len(addrs)
+        for d, a in enumerate(addrs):
+            t.seg[k].dst[d] = a
+    t.nseg = len(segs)
+    return t
 
 
 class LrSchedule(ctypes.Structure):
@@ -93,7 +123,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # JIGSAW_LIB: load another build of the same library (A/B timing of kernel changes, tools/ab.sh)
+    p = Path(path) if path else Path(os.environ.get("JIGSAW_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -117,6 +148,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_unpatchify": [vp, vp, i64, i64, i64, i64, i64, i64, vp],
         "jg_blend_loss": [vp] * 12 + [i64] * 6 + [f32, f32, vp, vp],
         "jg_adam": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp, vp],
+        "jg_adam_push": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp, ctypes.POINTER(PushTable), vp],
         "jg_step_increment": [vp, vp],
         "jg_sqnorm": [vp, i64, f32, vp, vp],
         "jg_opt_schedule": [vp, ctypes.POINTER(LrSchedule), i32, vp, f32, vp, vp, vp],

@@ -39,6 +39,13 @@ int resident_grid(Kern kernel, int block, int64_t work_blocks) {
   return static_cast<int>(work_blocks < 1 ? 1 : (work_blocks < cap ? work_blocks : cap));
 }
 
+// Column chunk per warp unit of the row-wise kernels: whole rows when the rows alone give every
+// SM 64 warps; otherwise 256 columns (one 16-byte vector per lane) so short row counts (Jigsaw
+// tiles) still fill the GPU.
+int64_t row_chunk(int64_t rows, int64_t cols) {
+  return rows >= static_cast<int64_t>(jg::num_sms()) * 64 ? (cols > 0 ? cols : 1) : 256;
+}
+
 int grid_for(int64_t work_items, int per_block) {
   int64_t b = (work_items + per_block - 1) / per_block;
   const int64_t cap = static_cast<int64_t>(jg::num_sms()) * 16;
@@ -153,22 +160,28 @@ __global__ void ln_moments_kernel(const float* __restrict__ x, float* __restrict
 __global__ void ln_apply_kernel(const float* __restrict__ x, const float* __restrict__ stats,
                                 const float* __restrict__ gamma, const float* __restrict__ beta, void* __restrict__ y,
                                 bool y_bf16, float* __restrict__ mean_rstd, int64_t rows, int64_t cols,
-                                float inv_ctotal, float eps, const Bcast bc) {
+                                float inv_ctotal, float eps, const Bcast bc, int64_t cw_arg) {
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const bool vec = (cols % 8 == 0);
-  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+  // vector path: warp unit = (row, column chunk of cw = k*256 columns; nch chunks per row);
+  // scalar path: warp per row
+  const int64_t cw = vec ? cw_arg : cols, nch = (cols + cw - 1) / cw;
+  for (int64_t u = wid; u < rows * nch; u += warps) {
+    const int64_t r = u / nch, ch = u - r * nch;
     const float mean = stats[2 * r] * inv_ctotal;
     const float var = stats[2 * r + 1] * inv_ctotal - mean * mean;
     const float rstd = 1.0f / sqrtf(var + eps);
-    if (lane == 0 && mean_rstd) {
+    if (ch == 0 && lane == 0 && mean_rstd) {
       mean_rstd[2 * r] = mean;
       mean_rstd[2 * r + 1] = rstd;
     }
     const float* xr = x + r * cols;
     const int64_t yo = r * cols;
     if (vec) {
-      for (int64_t c = lane * 8; c < cols; c += 256) {
+      const int64_t ce = (ch + 1) * cw < cols ? (ch + 1) * cw : cols;
+      for (int64_t c = ch * cw + lane * 8; c < ce; c += 256) {
         float v[8], gm[8], bt[8];
         jgd::load8(xr, c, false, v);
         jgd::load8(gamma, c, false, gm);
@@ -187,17 +200,21 @@ __global__ void ln_apply_kernel(const float* __restrict__ x, const float* __rest
 
 __global__ void ln_bwd_moments_kernel(const float* __restrict__ x, const float* __restrict__ g,
                                       const float* __restrict__ gamma, const float* __restrict__ mean_rstd,
-                                      float* __restrict__ bstats, int64_t rows, int64_t cols) {
+                                      float* __restrict__ bstats, int64_t rows, int64_t cols, int64_t cw_arg) {
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const bool vec = (cols % 8 == 0);
-  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+  const int64_t cw = vec ? cw_arg : cols, nch = (cols + cw - 1) / cw;  // vector path: (row, chunk) units
+  for (int64_t u = wid; u < rows * nch; u += warps) {
+    const int64_t r = u / nch, ch = u - r * nch;
     const float mean = mean_rstd[2 * r], rstd = mean_rstd[2 * r + 1];
     const float* xr = x + r * cols;
     const float* gr = g + r * cols;
     float sh = 0.f, shx = 0.f;
     if (vec) {
-      for (int64_t c = lane * 8; c < cols; c += 256) {
+      const int64_t ce = (ch + 1) * cw < cols ? (ch + 1) * cw : cols;
+      for (int64_t c = ch * cw + lane * 8; c < ce; c += 256) {
         float xv[8], gv[8], gm[8];
         jgd::load8(xr, c, false, xv);
         jgd::load8(gr, c, false, gv);
@@ -225,9 +242,10 @@ __global__ void ln_bwd_moments_kernel(const float* __restrict__ x, const float* 
   }
 }
 
-// 2-D tiled: block = 256 threads over 4*256 = 1024 columns, ROWS_PER_BLOCK rows.
-// Column partials of dgamma / dbeta stay in registers; one atomic per column per block.
-constexpr int LNB_ROWS = 64;
+// 2-D tiled: block = 256 threads over 4*256 = 1024 columns, LNB_ROWS rows, processed LNB_U rows
+// at a time (all their loads issued before any math or store: LNB_U x 3 16-byte loads in flight
+// per thread). Column partials of dgamma / dbeta stay in registers; one atomic per column per block.
+constexpr int LNB_ROWS = 64, LNB_U = 4;
 __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __restrict__ g,
                                     const float* __restrict__ gamma, const float* __restrict__ mean_rstd,
                                     const float* __restrict__ bstats, const float* __restrict__ resid,
@@ -239,77 +257,129 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
   if (c0 >= cols) return;
   const int64_t r1 = r0 + LNB_ROWS < rows ? r0 + LNB_ROWS : rows;
   const int nc = cols - c0 >= 4 ? 4 : static_cast<int>(cols - c0);
+  const bool v4 = nc == 4 && (cols % 4 == 0);
   float gm[4], dg[4] = {0, 0, 0, 0}, db[4] = {0, 0, 0, 0};
+#pragma unroll
   for (int j = 0; j < 4; ++j) gm[j] = j < nc ? gamma[c0 + j] : 0.f;
-  for (int64_t r = r0; r < r1; ++r) {
-    const float mean = mean_rstd[2 * r], rstd = mean_rstd[2 * r + 1];
-    const float msh = bstats[2 * r] * inv_ctotal, mshx = bstats[2 * r + 1] * inv_ctotal;
-    const int64_t o = r * cols + c0;
-    float xv[4], gv[4], rv[4] = {0, 0, 0, 0}, ov[4];
-    if (nc == 4 && (cols % 4 == 0)) {
-      const float4 a = *reinterpret_cast<const float4*>(x + o);
-      const float4 b = *reinterpret_cast<const float4*>(g + o);
-      xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
-      gv[0] = b.x; gv[1] = b.y; gv[2] = b.z; gv[3] = b.w;
-      if (resid) {
-        const float4 c = *reinterpret_cast<const float4*>(resid + o);
-        rv[0] = c.x; rv[1] = c.y; rv[2] = c.z; rv[3] = c.w;
-      }
-    } else {
-      for (int j = 0; j < 4; ++j) {
-        xv[j] = j < nc ? x[o + j] : 0.f;
-        gv[j] = j < nc ? g[o + j] : 0.f;
-        rv[j] = (resid && j < nc) ? resid[o + j] : 0.f;
+  for (int64_t rb = r0; rb < r1; rb += LNB_U) {
+    float xv[LNB_U][4], gv[LNB_U][4], rv[LNB_U][4];
+#pragma unroll
+    for (int u = 0; u < LNB_U; ++u) {
+      const int64_t r = rb + u;
+      const int64_t o = r * cols + c0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) xv[u][j] = gv[u][j] = rv[u][j] = 0.f;
+      if (r >= r1) continue;
+      if (v4) {
+        const float4 a = *reinterpret_cast<const float4*>(x + o);
+        const float4 b = *reinterpret_cast<const float4*>(g + o);
+        xv[u][0] = a.x; xv[u][1] = a.y; xv[u][2] = a.z; xv[u][3] = a.w;
+        gv[u][0] = b.x; gv[u][1] = b.y; gv[u][2] = b.z; gv[u][3] = b.w;
+        if (resid) {
+          const float4 c = *reinterpret_cast<const float4*>(resid + o);
+          rv[u][0] = c.x; rv[u][1] = c.y; rv[u][2] = c.z; rv[u][3] = c.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < nc) {
+            xv[u][j] = x[o + j];
+            gv[u][j] = g[o + j];
+            rv[u][j] = resid ? resid[o + j] : 0.f;
+          }
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float xh = (xv[j] - mean) * rstd;
-      const float h = gv[j] * gm[j];
-      ov[j] = rv[j] + rstd * (h - msh - xh * mshx);
-      dg[j] += gv[j] * xh;
-      db[j] += gv[j];
-    }
-    if (nc == 4 && (cols % 4 == 0)) {
-      *reinterpret_cast<float4*>(out + o) = make_float4(ov[0], ov[1], ov[2], ov[3]);
-      if (out_bf16) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(ov[0], ov[1]), hi = __floats2bfloat162_rn(ov[2], ov[3]);
-        uint2 raw;
-        raw.x = *reinterpret_cast<uint32_t*>(&lo);
-        raw.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(out_bf16 + o) = raw;
-        for (int i = 0; i < bc.n; ++i) *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(bc.p[i]) + o) = raw;
-      }
-    } else {
-      for (int j = 0; j < nc; ++j) {
-        out[o + j] = ov[j];
-        if (out_bf16) {
-          out_bf16[o + j] = __float2bfloat16_rn(ov[j]);
-          for (int i = 0; i < bc.n; ++i) reinterpret_cast<__nv_bfloat16*>(bc.p[i])[o + j] = __float2bfloat16_rn(ov[j]);
+    for (int u = 0; u < LNB_U; ++u) {
+      const int64_t r = rb + u;
+      if (r >= r1) continue;
+      const float mean = mean_rstd[2 * r], rstd = mean_rstd[2 * r + 1];
+      const float msh = bstats[2 * r] * inv_ctotal, mshx = bstats[2 * r + 1] * inv_ctotal;
+      const int64_t o = r * cols + c0;
+      float ov[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float xh = (xv[u][j] - mean) * rstd;
+        const float h = gv[u][j] * gm[j];
+        ov[j] = rv[u][j] + rstd * (h - msh - xh * mshx);
+        if (j < nc) {
+          dg[j] += gv[u][j] * xh;
+          db[j] += gv[u][j];
         }
       }
+      if (v4) {
+        *reinterpret_cast<float4*>(out + o) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+        if (out_bf16) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(ov[0], ov[1]), hi = __floats2bfloat162_rn(ov[2], ov[3]);
+          uint2 raw;
+          raw.x = *reinterpret_cast<uint32_t*>(&lo);
+          raw.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(out_bf16 + o) = raw;
+          for (int i = 0; i < bc.n; ++i) *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(bc.p[i]) + o) = raw;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < nc) {
+            out[o + j] = ov[j];
+            if (out_bf16) {
+              out_bf16[o + j] = __float2bfloat16_rn(ov[j]);
+              for (int i = 0; i < bc.n; ++i) reinterpret_cast<__nv_bfloat16*>(bc.p[i])[o + j] = __float2bfloat16_rn(ov[j]);
+            }
+          }
+      }
     }
   }
-  for (int j = 0; j < nc; ++j) {
-    if (dgamma) atomicAdd(dgamma + c0 + j, dg[j]);
-    if (dbeta) atomicAdd(dbeta + c0 + j, db[j]);
-  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (j < nc) {
+      if (dgamma) atomicAdd(dgamma + c0 + j, dg[j]);
+      if (dbeta) atomicAdd(dbeta + c0 + j, db[j]);
+    }
   if (bc.n) __threadfence_system();
 }
 
 // ---------------------------------------------------------------- bias-grad reductions
-constexpr int CS_ROWS = 128;
+// colsum: block = 8 warps over 256 columns (8 per lane, 16-byte loads) x CS_ROWS rows; warp w
+// takes rows w, w+8, ... (CS_ROWS/8 independent loads in flight per thread); the 8 warp
+// partials meet in shared memory and one atomic per column per block goes to global.
+constexpr int CS_ROWS = 256;
 __global__ void colsum_kernel(const void* __restrict__ x, bool bf16, float* __restrict__ out, int64_t rows,
-                              int64_t cols, int64_t ldx) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+                              int64_t cols, int64_t ldx, bool vec) {
+  __shared__ float part[8][8 * 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = blockIdx.x * (int64_t)256 + lane * 8;
   const int64_t r0 = blockIdx.y * (int64_t)CS_ROWS;
   const int64_t r1 = r0 + CS_ROWS < rows ? r0 + CS_ROWS : rows;
-  float s = 0.f;
-  for (int64_t r = r0; r < r1; ++r) s += jgd::load1(x, r * ldx + c, bf16);
-  atomicAdd(out + c, s);
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (c0 < cols) {
+    if (vec) {
+#pragma unroll 4
+      for (int64_t r = r0 + w; r < r1; r += 8) {
+        float t[8];
+        jgd::load8(x, r * ldx + c0, bf16, t);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] += t[j];
+      }
+    } else {
+      for (int64_t r = r0 + w; r < r1; r += 8)
+        for (int j = 0; j < 8; ++j)
+          if (c0 + j < cols) s[j] += jgd::load1(x, r * ldx + c0 + j, bf16);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[w][j * 32 + lane] = s[j];
+  __syncthreads();
+  if (w == 0 && c0 < cols) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += part[k][j * 32 + lane];
+      if (c0 + j < cols) atomicAdd(out + c0 + j, t);
+    }
+  }
 }
-
 __global__ void rowsum_kernel(const void* __restrict__ x, bool bf16, float* __restrict__ out, int64_t rows,
                               int64_t cols, int64_t ldx) {
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -442,7 +512,7 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
                                   float* __restrict__ g_blend, float* __restrict__ g_dec_f32,
                                   __nv_bfloat16* __restrict__ g_dec_bf16, int64_t batch, int64_t lat, int64_t lon,
                                   int chans, int pl, int pw_rt, float inv_count, float loss_scale, const Bcast bc) {
-  __shared__ float s_gb[MAX_CH];
+  __shared__ float s_part[1024];  // per-thread blend-gradient partials (blockDim <= 1024)
   __shared__ float s_loss[32];
   const int pw = PW > 0 ? PW : pw_rt;
   const int C = chans;
@@ -452,8 +522,6 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
   const bool want_grad = (g_ext != nullptr) || (target != nullptr);
   const int act = (static_cast<int>(blockDim.x) / C) * C;  // > 0: host guarantees C <= blockDim
   const int t0 = static_cast<int>(threadIdx.x);
-  for (int c = t0; c < C; c += blockDim.x) s_gb[c] = 0.f;
-  __syncthreads();
   float lsum = 0.f, gb = 0.f;
   if (t0 < act) {
     const int my_c = t0 % C;
@@ -515,8 +583,8 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
           }
       }
     }
-    if (want_grad) atomicAdd(&s_gb[my_c], gb);
   }
+  s_part[t0] = gb;
   lsum = warp_sum(lsum);
   if ((threadIdx.x & 31) == 0) s_loss[threadIdx.x >> 5] = lsum;
   __syncthreads();
@@ -525,16 +593,41 @@ __global__ void blend_loss_kernel(const float* __restrict__ dec_tok, const float
     v = warp_sum(v);
     if (threadIdx.x == 0 && loss_sum && target && !g_ext) atomicAdd(loss_sum, v * inv_count);
   }
-  if (g_blend && want_grad)
-    for (int c = t0; c < C; c += blockDim.x) atomicAdd(g_blend + c, s_gb[c]);
+  if (g_blend && want_grad)  // fixed-order sum of the act / C threads that own channel c
+    for (int c = t0; c < C; c += blockDim.x) {
+      float t = 0.f;
+      for (int k = c; k < act; k += C) t += s_part[k];
+      atomicAdd(g_blend + c, t);
+    }
   if (bc.n) __threadfence_system();
 }
 
 // ---------------------------------------------------------------- Adam
+// Segments of the range whose bf16 copy is also pushed to peer gather slots (jg_adam_push).
+__device__ __forceinline__ void push_bf16x4(const jg_push_table& t, int64_t e, uint2 raw) {
+  for (int k = 0; k < t.nseg; ++k) {
+    const jg_push_seg& sg = t.seg[k];
+    if (e >= sg.start && e < sg.start + sg.len) {
+      for (int d = 0; d < sg.ndst; ++d)
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sg.dst[d]) + (e - sg.start)) = raw;
+      return;
+    }
+  }
+}
+__device__ __forceinline__ void push_bf16x1(const jg_push_table& t, int64_t e, __nv_bfloat16 h) {
+  for (int k = 0; k < t.nseg; ++k) {
+    const jg_push_seg& sg = t.seg[k];
+    if (e >= sg.start && e < sg.start + sg.len) {
+      for (int d = 0; d < sg.ndst; ++d) reinterpret_cast<__nv_bfloat16*>(sg.dst[d])[e - sg.start] = h;
+      return;
+    }
+  }
+}
+
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, __nv_bfloat16* __restrict__ pb, int64_t n, float lr, float b1,
                             float b2, float eps, const int32_t* __restrict__ step, const float* __restrict__ gscale,
-                            const float* __restrict__ lr_dev) {
+                            const float* __restrict__ lr_dev, const jg_push_table push) {
   const int t = *step;
   if (lr_dev) lr = *lr_dev;
   const float bc1 = 1.0f / (1.0f - powf(b1, (float)t));
@@ -563,6 +656,7 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
       raw.x = *reinterpret_cast<uint32_t*>(&lo);
       raw.y = *reinterpret_cast<uint32_t*>(&hi);
       reinterpret_cast<uint2*>(pb)[i] = raw;
+      if (push.nseg) push_bf16x4(push, 4 * i, raw);
     }
   }
   // scalar tail
@@ -572,7 +666,9 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     v[i] = b2 * v[i] + (1.0f - b2) * gj * gj;
     p[i] -= lr * (m[i] * bc1) / (sqrtf(v[i] * bc2) + eps);
     if (pb) pb[i] = __float2bfloat16_rn(p[i]);
+    if (pb && push.nseg) push_bf16x1(push, i, __float2bfloat16_rn(p[i]));
   }
+  if (push.nseg) __threadfence_system();  // peer copies complete before the next group barrier
 }
 
 __global__ void step_inc_kernel(int32_t* counter) { *counter += 1; }
@@ -705,38 +801,57 @@ __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t 
   }
 }
 
+// Vector path: warp unit = (row, 256-column chunk), so even a few thousand rows give tens of
+// thousands of independent units (enough loads in flight without long per-warp row loops);
+// LN-moment partials are warp-reduced per unit and added with one atomic pair per unit.
 __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
   const int64_t b = blockIdx.y;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < a.m; r += warps) {
-    const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
-    float s1 = 0.f, s2 = 0.f;
-    if (vec) {
-      for (int64_t c = lane * 8; c < a.n; c += 256) {
+  if (vec) {
+    const int64_t nch = (a.n + 255) / 256;
+    for (int64_t u = wid; u < a.m * nch; u += warps) {
+      const int64_t r = u / nch, c = (u - r * nch) * 256 + lane * 8;
+      const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
+      float s1 = 0.f, s2 = 0.f;
+      if (c < a.n) {
         float v[8];
         epi_apply8(a, b, r, c, rb, v, s1, s2);
       }
-    } else {
-      for (int64_t c = lane; c < a.n; c += 32) {
-        float v = 0.f;
-        if (a.nplanes > 1) {
-          for (int pl = 0; pl < a.nplanes; ++pl) v += jgd::load1(a.acc, pl * a.a_bs + r * a.lda + c, a.acc_bf16);
-        } else {
-          v = jgd::load1(a.acc, b * a.a_bs + r * a.lda + c, a.acc_bf16);
+      if (a.epi & JG_EPI_STATS) {
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        if (lane == 0) {
+          atomicAdd(a.stats + b * a.stats_bs + 2 * r, s1);
+          atomicAdd(a.stats + b * a.stats_bs + 2 * r + 1, s2);
         }
-        v = v * a.alpha + rb;
-        if (a.epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
-        if (a.epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
-        if (a.epi & JG_EPI_GELU_BWD) v *= jgd::gelu_grad_f(jgd::load1(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16));
-        const int64_t od = b * a.d_bs + r * a.ldd + c;
-        if (a.epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
-        s1 += v;
-        s2 += v * v;
-        if (a.d) store1_bc(a.d, a.dbc, od, a.d_bf16, v);
-        if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
-          store1_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
       }
+    }
+    if (a.dbc.n || a.d2bc.n) __threadfence_system();
+    return;
+  }
+  for (int64_t r = wid; r < a.m; r += warps) {
+    const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
+    float s1 = 0.f, s2 = 0.f;
+    for (int64_t c = lane; c < a.n; c += 32) {
+      float v = 0.f;
+      if (a.nplanes > 1) {
+        for (int pl = 0; pl < a.nplanes; ++pl) v += jgd::load1(a.acc, pl * a.a_bs + r * a.lda + c, a.acc_bf16);
+      } else {
+        v = jgd::load1(a.acc, b * a.a_bs + r * a.lda + c, a.acc_bf16);
+      }
+      v = v * a.alpha + rb;
+      if (a.epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
+      if (a.epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
+      if (a.epi & JG_EPI_GELU_BWD) v *= jgd::gelu_grad_f(jgd::load1(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16));
+      const int64_t od = b * a.d_bs + r * a.ldd + c;
+      if (a.epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
+      s1 += v;
+      s2 += v * v;
+      if (a.d) store1_bc(a.d, a.dbc, od, a.d_bf16, v);
+      if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
+        store1_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
     }
     if (a.epi & JG_EPI_STATS) {
       s1 = warp_sum(s1);
@@ -853,9 +968,11 @@ int jg_ln_apply(const float* x, const float* stats, const float* gamma, const fl
   JG_SHAPE_CHECK(rows >= 0 && cols > 0 && c_total >= cols, "jg_ln_apply: bad shape");
   JG_SHAPE_CHECK(al16(x) && al16(y) && al16(gamma) && al16(beta), "jg_ln_apply: pointers must be 16B aligned");
   if (rows == 0) return JG_OK;
-  ln_apply_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(x, stats, gamma, beta, y, y_type == JG_BF16,
+  const int64_t cw = row_chunk(rows, cols);
+  const int64_t lnu = rows * ((cols + cw - 1) / cw);
+  ln_apply_kernel<<<resident_grid(ln_apply_kernel, 256, (lnu + 7) / 8), 256, 0, (cudaStream_t)stream>>>(x, stats, gamma, beta, y, y_type == JG_BF16,
                                                                       mean_rstd, rows, cols, 1.0f / (float)c_total, eps,
-                                                                      to_bcast(y_bcast));
+                                                                      to_bcast(y_bcast), cw);
   JG_LAUNCH_CHECK("ln_apply");
   return JG_OK;
 }
@@ -865,7 +982,9 @@ int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const 
   JG_SHAPE_CHECK(rows >= 0 && cols > 0, "jg_ln_bwd_moments: bad shape");
   JG_SHAPE_CHECK(al16(x) && al16(g) && al16(gamma), "jg_ln_bwd_moments: pointers must be 16B aligned");
   if (rows == 0) return JG_OK;
-  ln_bwd_moments_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(x, g, gamma, mean_rstd, bstats, rows, cols);
+  const int64_t cw = row_chunk(rows, cols);
+  const int64_t lnu = rows * ((cols + cw - 1) / cw);
+  ln_bwd_moments_kernel<<<resident_grid(ln_bwd_moments_kernel, 256, (lnu + 7) / 8), 256, 0, (cudaStream_t)stream>>>(x, g, gamma, mean_rstd, bstats, rows, cols, cw);
   JG_LAUNCH_CHECK("ln_bwd_moments");
   return JG_OK;
 }
@@ -891,8 +1010,9 @@ int jg_ln_bwd_apply(const float* x, const float* g, const float* gamma, const fl
 int jg_colsum(const void* x, int32_t x_type, float* out, int64_t rows, int64_t cols, int64_t ldx, void* stream) {
   JG_SHAPE_CHECK(rows >= 0 && cols > 0 && ldx >= cols, "jg_colsum: bad shape");
   if (rows == 0) return JG_OK;
+  const bool vec = cols % 8 == 0 && ldx % 8 == 0 && al16(x);
   dim3 grid((unsigned)((cols + 255) / 256), (unsigned)((rows + CS_ROWS - 1) / CS_ROWS));
-  colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, x_type == JG_BF16, out, rows, cols, ldx);
+  colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, x_type == JG_BF16, out, rows, cols, ldx, vec);
   JG_LAUNCH_CHECK("colsum");
   return JG_OK;
 }
@@ -989,16 +1109,36 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
   return JG_OK;
 }
 
-int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, float lr, float beta1, float beta2,
-            float eps, const int32_t* step_dev, const float* grad_scale_dev, const float* lr_dev, void* stream) {
+int jg_adam_push(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, float lr, float beta1,
+                 float beta2, float eps, const int32_t* step_dev, const float* grad_scale_dev, const float* lr_dev,
+                 const jg_push_table* push, void* stream) {
   JG_SHAPE_CHECK(n >= 0 && step_dev, "jg_adam: bad arguments");
   JG_SHAPE_CHECK(al16(p) && al16(g) && al16(m) && al16(v) && (!p_bf16 || (reinterpret_cast<uintptr_t>(p_bf16) & 7u) == 0),
                  "jg_adam: buffers must be 16B aligned");
+  jg_push_table t{};
+  if (push && push->nseg > 0) {
+    JG_SHAPE_CHECK(p_bf16 && push->nseg <= JG_MAX_PUSH_SEGS, "jg_adam_push: needs the bf16 copy, <= %d segments",
+                   JG_MAX_PUSH_SEGS);
+    for (int k = 0; k < push->nseg; ++k) {
+      const jg_push_seg& sg = push->seg[k];
+      JG_SHAPE_CHECK(sg.start >= 0 && sg.len >= 0 && sg.start + sg.len <= n && sg.start % 4 == 0 && sg.len % 4 == 0 &&
+                         sg.ndst >= 0 && sg.ndst <= 4,
+                     "jg_adam_push: bad segment %d", k);
+      for (int d = 0; d < sg.ndst; ++d)
+        JG_SHAPE_CHECK((reinterpret_cast<uintptr_t>(sg.dst[d]) & 7u) == 0, "jg_adam_push: dst must be 8B aligned");
+    }
+    t = *push;
+  }
   if (n == 0) return JG_OK;
   adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
-      p, g, m, v, (__nv_bfloat16*)p_bf16, n, lr, beta1, beta2, eps, step_dev, grad_scale_dev, lr_dev);
+      p, g, m, v, (__nv_bfloat16*)p_bf16, n, lr, beta1, beta2, eps, step_dev, grad_scale_dev, lr_dev, t);
   JG_LAUNCH_CHECK("adam");
   return JG_OK;
+}
+
+int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, float lr, float beta1, float beta2,
+            float eps, const int32_t* step_dev, const float* grad_scale_dev, const float* lr_dev, void* stream) {
+  return jg_adam_push(p, g, m, v, p_bf16, n, lr, beta1, beta2, eps, step_dev, grad_scale_dev, lr_dev, nullptr, stream);
 }
 
 int jg_opt_schedule(const int32_t* step_dev, const jg_lr_schedule* sched, int32_t nsched, const float* sqsum_dev,
@@ -1053,12 +1193,13 @@ int jg_epilogue(const jg_gemm_desc* g, const void* acc, int32_t acc_type, int64_
   a.stats = g->stats; a.stats_bs = g->stats_bstride;
   a.dbc = to_bcast(&g->d_bcast);
   a.d2bc = to_bcast(&g->d2_bcast);
-  dim3 grid((unsigned)grid_for(g->m, 8), (unsigned)g->batch);
   auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   const bool vec = g->n % 8 == 0 && lda % 8 == 0 && acc_bstride % 8 == 0 && g->ldd % 8 == 0 && g->ldd2 % 8 == 0 &&
                    g->ldr % 8 == 0 && g->ldp % 8 == 0 && g->bias_bstride % 8 == 0 && a16(acc) && a16(g->d) &&
                    a16(g->d2) && a16(g->bias) && a16(g->resid) && a16(g->pre) && g->d_bstride % 8 == 0 &&
                    g->r_bstride % 8 == 0 && g->p_bstride % 8 == 0 && g->d2_bstride % 8 == 0;
+  const int64_t units = vec ? g->m * ((g->n + 255) / 256) : g->m;  // warp units per batch entry
+  dim3 grid((unsigned)resident_grid(epilogue_kernel, 256, (units + 7) / 8), (unsigned)g->batch);
   epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a, vec);
   JG_LAUNCH_CHECK("epilogue");
   return JG_OK;

@@ -12,6 +12,8 @@ and 482-490 (see train.py).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -57,6 +59,14 @@ class TrainStep:
         self._pinned_loss = torch.zeros(1, dtype=torch.float32, pin_memory=dev.type == "cuda")
         self._h2d_bytes = 2 * self.ws.xin.numel() * 4
         self._d2h_bytes = 4
+        # Jigsaw R > 1 over symmetric memory: Adam stores each channel-mixing weight's new bf16
+        # copy straight into the column group's panel slots (jg_adam_push), so the next forward
+        # replaces the per-panel all-gathers with one barrier. The slots then hold the weights as
+        # of this TrainStep's last update: `_panel_version` tracks model.weights_version and a
+        # stale step (external weight edit, or another TrainStep's update) re-gathers eagerly.
+        self.push_panels = (model.ctx.n > 1 and model.R > 1 and not self.fused_adam
+                            and os.environ.get("JIGSAW_PANEL_PUSH", "1") == "1")
+        self._panel_version = None
 
     # -- the step body --------------------------------------------------------------------
     def _body(self) -> None:
@@ -74,7 +84,11 @@ class TrainStep:
                 f.grad[lo:hi].zero_()
         else:
             m.zero_grads()
-        m._forward(ws)
+        m._panels_pushed = self._pushing()
+        try:
+            m._forward(ws)
+        finally:
+            m._panels_pushed = False
 
     def _body_bwd(self) -> None:
         """Loss against the target, backward, gradient sync, Adam."""
@@ -114,9 +128,21 @@ class TrainStep:
                     K.sqnorm(f.grad[lo:hi], self.sqsum, w)
         m.ctx.all_reduce_all(self.sqsum)
 
+    def _pushing(self) -> bool:
+        """Adam pushes the weight panels (and the forward only barriers) in this step body."""
+        g = getattr(self.ws, "grid", None)
+        return (self.push_panels and not self._dry and g is not None and g.kind == "symm"
+                and bool(g.panel_names) and self.model.flat.op is not self.model.flat.master)
+
     def _adam(self) -> None:
+        from .jigsaw_grid import panel_push_segments
         f, a = self.model.flat, self.adam
         op_copy = f.op if f.op is not f.master else None
+        push = self._pushing()
+        if push:
+            # no column-group member may still be reading this step's panels (the encoder's dW
+            # GEMM is the last reader) when the pushes land in its slots
+            self.ws.grid.col.barrier()
         for i, (cls, (lo, hi)) in enumerate(f.class_range.items()):
             if self.fused_adam:
                 lo, hi = f.vec_range(cls)
@@ -125,7 +151,25 @@ class TrainStep:
             K.adam(f.master[lo:], f.grad[lo:], f.m[lo:], f.v[lo:], None if op_copy is None else op_copy[lo:],
                    hi - lo, a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count,
                    grad_scale=self.grad_scale if self.clip is not None else None,
-                   lr_dev=self.lr_dev[i:i + 1] if self.scheduled else None)
+                   lr_dev=self.lr_dev[i:i + 1] if self.scheduled else None,
+                   push=panel_push_segments(self.model, self.ws.grid, lo, hi) if push else None)
+
+    def _refresh_panels(self) -> None:
+        """Before a step whose forward relies on pushed panels: if the weights changed since this
+        TrainStep's last update (init, checkpoint load, another TrainStep), gather them now."""
+        m = self.model
+        if not self._pushing():
+            return
+        v = getattr(m, "weights_version", 0)
+        if self._panel_version != v:
+            from .jigsaw_grid import gather_panels
+            gather_panels(m, self.ws.grid)
+
+    def _updated(self) -> None:
+        """After a step's Adam: the model changed and this TrainStep's panel slots hold it."""
+        m = self.model
+        m.weights_version = getattr(m, "weights_version", 0) + 1
+        self._panel_version = m.weights_version
 
     def capture(self) -> None:
         """Warm up on a side stream with a dry step (forward, loss, backward, gradient sync: no
@@ -159,17 +203,20 @@ class TrainStep:
         if self.use_graph:
             if self.graph is None:
                 self.capture()
+            self._refresh_panels()
             self.graph[0].replay()
             if target_ready is not None:
                 torch.cuda.current_stream().wait_event(target_ready)
             self.graph[1].replay()
         else:
             before = _lib.launch_count()
+            self._refresh_panels()
             self._body_fwd()
             if target_ready is not None:
                 torch.cuda.current_stream().wait_event(target_ready)
             self._body_bwd()
             self.launches_per_step = _lib.launch_count() - before
+        self._updated()
         return self.ws.loss
 
     def __call__(self, x: torch.Tensor, target: torch.Tensor) -> float:

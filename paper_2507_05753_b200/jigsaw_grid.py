@@ -118,6 +118,35 @@ def gather_panels(m, g) -> None:
         g.col.ag(m.params[name].op, slot=f"panel:{name}")
 
 
+def panel_push_segments(m, g, lo: int, hi: int):
+    """Adam-side weight-panel gather (symmetric-memory transport, R > 1): for the flat range
+    [lo, hi) of one Adam call, the channel-mixing weights in it as (start - lo, numel, addrs) —
+    addrs = this rank's plane of the weight's panel slot in every column-group member's arena
+    (own included), where the optimiser stores the new bf16 operand copy. The next forward then
+    only needs one column-group barrier instead of one copy + barrier per panel."""
+    if g.kind != "symm" or g.col is None or not g.panel_names:
+        return []
+    f = m.flat
+    es = f.op.element_size()
+    base = f.op.data_ptr()
+    segs = []
+    for name in g.panel_names:
+        op = m.params[name].op
+        start = (op.data_ptr() - base) // es
+        if not lo <= start < hi:
+            continue
+        nbytes = op.numel() * es
+        off = g.col._slot_off(f"panel:{name}", 0, nbytes) + g.col.idx * nbytes
+        segs.append((start - lo, op.numel(), [g.col.base[j] + off for j in range(g.col.G)]))
+    return segs
+
+
+def panels_ready(m, g) -> None:
+    """Forward prologue when the previous step's Adam pushed the panels: one barrier publishes
+    every member's pushes (their Adam kernels end with a system fence)."""
+    g.col.barrier()
+
+
 def _wgrad_planes(m, g, wname, acc, nplanes, plane_stride, numel):
     """Weight gradient that arrived as reduce-scatter planes: sum them into the gradient sink."""
     if nplanes == 1 and acc.dtype == F32:
@@ -269,7 +298,10 @@ def forward_grid(m, ws) -> None:
     lat, lon = m.local_grid
     od = m.op_dtype
     ws.stats.zero_()
-    gather_panels(m, g)
+    if getattr(m, "_panels_pushed", False) and g.kind == "symm" and g.panel_names:
+        panels_ready(m, g)
+    else:
+        gather_panels(m, g)
     K.patchify(ws.xin, ws.xp, B, lat, lon, m.local_vars, cfg.patch[0], cfg.patch[1])
     chan_fwd(m, g, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, epi=E_BCOL | E_ST, bias=p["enc.b"].data,
              d=ws.res[0], stats=ws.st1[0])

@@ -235,9 +235,12 @@ class WeatherMixerModel:
         self.sync_operand_copies()
 
     def sync_operand_copies(self):
-        """Refresh the bf16 GEMM-operand copy of the master weights (after init / external edits)."""
+        """Refresh the bf16 GEMM-operand copy of the master weights (after init / external edits).
+        Collective in effect: every rank calls it, and `weights_version` (which tells a TrainStep
+        that its optimiser-pushed weight panels are stale) advances on every rank."""
         if self.flat.op is not self.flat.master:
             K.cast_bf16(self.flat.master, self.flat.op)
+        self.weights_version = getattr(self, "weights_version", 0) + 1
 
     # -- introspection (model.py:462-529) -------------------------------------------------
     @property
@@ -264,7 +267,7 @@ class WeatherMixerModel:
         li = self.layouts[name].to_local_index(self.ctx.pos, idx)
         if li is not None:
             self.params[name].data[li] = value
-            self.sync_operand_copies()
+        self.sync_operand_copies()  # every rank: keeps weights_version equal across ranks
 
     def get_param_entry(self, name, idx):
         li = self.layouts[name].to_local_index(self.ctx.pos, idx)

@@ -292,7 +292,7 @@ def opt_schedule(step, scheds, sqsum, clip_norm, lr_out, grad_scale):
         grad_scale.fill_(f)
 
 
-def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None):
+def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None, push=None):
     t = int(step.item())
     if lr_dev is not None:
         lr = float(lr_dev.item())
@@ -304,6 +304,8 @@ def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_d
     pv.sub_(lr * (mv / (1 - beta1 ** t)) / (torch.sqrt(vv / (1 - beta2 ** t)) + eps))
     if p_op is not None:
         p_op.reshape(-1)[:n].copy_(pv.to(p_op.dtype))
+    for start, ln, addrs in push or []:
+        _bcast_copy(p_op.reshape(-1)[start:start + ln], addrs)
 
 
 def step_increment(counter):

@@ -38,7 +38,8 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
         torch.set_num_threads(1)
         import cpu_kernels
         cpu_kernels.install()
-        if (opts or {}).get("transport") == "shm":
+        opts = opts or {}
+        if opts.get("transport") == "shm":
             import shm_transport
             shm_transport.install()
         from oracle import model as om
@@ -46,12 +47,13 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
         z = np.load(os.path.join(GOLD, "wm_golden.npz"))
         meta = json.load(open(os.path.join(GOLD, "comm_golden.json")))
         comm = Communicator.from_env(backend="gloo") if world > 1 else Communicator.local()
-        opts = opts or {}
         n_mp = opts.get("mp", world)
         k = rank // n_mp
         ctx = MpContext(comm, list(range(k * n_mp, (k + 1) * n_mp)))
         cfg = ModelConfig.from_dict(meta["config"])
-        model = WeatherMixerModel(ctx, cfg, seed=0, dtype="f32", device="cpu")
+        if "panel_push" in opts:
+            os.environ["JIGSAW_PANEL_PUSH"] = opts["panel_push"]
+        model = WeatherMixerModel(ctx, cfg, seed=0, dtype=opts.get("dtype", "f32"), device="cpu")
         oc = om.Config(**{**meta["config"], "grid": tuple(meta["config"]["grid"]), "patch": tuple(meta["config"]["patch"])})
         x = z["x"][:1] if r > 1 else z["x"]
         g = z["g_out"][:1] if r > 1 else z["g_out"]
@@ -111,6 +113,22 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
                 p_res = {k_: p.data.numpy().copy() for k_, p in model2.params.items()}
                 out_q.put({"pos": ctx.pos, "rank": rank, "same": same, "cont": cont, "resumed": resumed,
                            "step": hdr["step"], "params_equal": all(np.array_equal(p_cont[k_], p_res[k_]) for k_ in p_cont)})
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+                dist.destroy_process_group()
+            return
+        if mode == "pushcmp":
+            from paper_2507_05753_b200.engine import TrainStep
+            tl = om.local_sample(oc, z["g_out"][:1] * 0.5, ctx.R, ctx.C, ctx.r, ctx.c)
+            step = TrainStep(model, batch=1, graph=False)
+            step.ws.xin.copy_(torch.tensor(xl[:1], dtype=torch.float32))
+            step.target.copy_(torch.tensor(tl, dtype=torch.float32))
+            losses = [float(step.run_device().item()) for _ in range(2)]
+            model.set_param_entry("block0.ch1.w", (1, 2), 0.25)  # external edit: pushed panels go stale
+            losses += [float(step.run_device().item()) for _ in range(2)]
+            out_q.put({"pos": ctx.pos, "rank": rank, "losses": losses, "pushing": step._pushing(),
+                       "params": {k_: p.data.float().numpy().copy() for k_, p in model.params.items()}})
             if world > 1:
                 import torch.distributed as dist
                 dist.barrier()
@@ -414,3 +432,19 @@ def test_trainer_rollout_finetune_matches_oracle(world):
     for d in res:
         assert np.allclose(d["losses"], losses, rtol=1e-5), (d["losses"], losses)
         _assert_updates(oc, d, params, p0)
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_adam_panel_push_matches_gathers(world):
+    """bf16 operand copies over the peer-memory transport: Adam storing each channel-mixing
+    weight's new copy into the column group's panel slots (jg_adam_push) gives bit-identical
+    training to re-gathering the panels every forward — including after an external weight edit,
+    which must trigger an eager re-gather."""
+    base = {"transport": "shm", "dtype": "bf16"}
+    push = _run(world, mode="pushcmp", opts={**base, "panel_push": "1"})
+    gath = _run(world, mode="pushcmp", opts={**base, "panel_push": "0"})
+    assert all(d["pushing"] for d in push) and not any(d["pushing"] for d in gath)
+    for a, b in zip(push, gath):
+        assert a["losses"] == b["losses"], (a["losses"], b["losses"])
+        for k in a["params"]:
+            assert np.array_equal(a["params"][k], b["params"][k]), k

@@ -38,3 +38,16 @@ def test_symmetric_memory_transport_matches_nccl(n):
            "--master-addr=127.0.0.1", "--master-port=29563", os.path.join(HERE, "transport_check.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert "TRANSPORT_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_captured_train_step_multi_gpu(n):
+    """Captured Jigsaw TrainStep: Adam-pushed weight panels are fresh after every step (bit-exact
+    vs an NCCL gather of the operand tiles), re-gathered after an external edit, and training
+    matches the gather-every-forward schedule."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29565", os.path.join(HERE, "train_mp_check.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert "TRAINMP_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]

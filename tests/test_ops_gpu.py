@@ -98,3 +98,62 @@ def test_blend_loss_kernel(cuda, rng, shape, patch, gdt):
         assert rel_err(gb.cpu().numpy(), gblend) < 1e-4
         if mode == "target":
             assert abs(lossd.item() - loss) / loss < 1e-5
+
+
+@pytest.mark.parametrize("rows,cols,ld,dt", [(8190, 2160, 2160, torch.bfloat16), (300, 72, 80, torch.float32),
+                                             (77, 13, 13, torch.float32), (1000, 264, 264, torch.float32)])
+def test_colsum_rowsum_kernels(cuda, rows, cols, ld, dt):
+    """Bias-gradient reductions (reference _sum_except, parallel.py:552-561): column and row sums
+    accumulate into fp32 outputs; vector (16-byte) and scalar paths, padded leading dimension."""
+    from paper_2507_05753_b200 import kernels as K
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x = torch.randn(rows, ld, device=cuda, generator=g).to(dt)
+    ref = x[:, :cols].double()
+    cs = torch.ones(cols, device=cuda)
+    K.colsum(x, cs, rows, cols, ld=ld)
+    assert rel_err(cs.cpu().numpy(), (ref.sum(0) + 1).cpu().numpy()) < 1e-5
+    rs = torch.ones(rows, device=cuda)
+    K.rowsum(x, rs, rows, cols, ld=ld)
+    assert rel_err(rs.cpu().numpy(), (ref.sum(1) + 1).cpu().numpy()) < 1e-5
+
+
+def test_epilogue_and_ln_kernels_tile_shapes(cuda):
+    """Jigsaw epilogue (planes summed + row bias + residual + LN moments; col bias + GELU) and the
+    layer-norm phases at 2x2-tile-like shapes with ragged column chunks, against fp64 torch."""
+    from paper_2507_05753_b200 import kernels as K, _lib
+    g = torch.Generator(device=cuda).manual_seed(7)
+    M, N = 515, 1080  # 1080 = 4 full 256-column chunks + a partial one
+    planes = torch.randn(2, M, N, device=cuda, generator=g).to(torch.bfloat16)
+    bias, resid = torch.randn(M, device=cuda, generator=g), torch.randn(M, N, device=cuda, generator=g)
+    d, st = torch.empty(M, N, device=cuda), torch.zeros(M, 2, device=cuda)
+    K.epilogue(planes, M, N, acc_bs=M * N, nplanes=2, epi=_lib.EPI_BIAS_ROW | _lib.EPI_RESID | _lib.EPI_STATS,
+               bias=bias, resid=resid, d=d, stats=st)
+    ref = planes.double().sum(0) + bias.double()[:, None] + resid.double()
+    assert rel_err(d.cpu().numpy(), ref.cpu().numpy()) < 1e-6
+    assert rel_err(st[:, 0].cpu().numpy(), ref.sum(1).cpu().numpy()) < 1e-5
+    assert rel_err(st[:, 1].cpu().numpy(), (ref * ref).sum(1).cpu().numpy()) < 1e-5
+    cb = torch.randn(N, device=cuda, generator=g)
+    h, a = torch.empty(M, N, device=cuda), torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    K.epilogue(planes, M, N, acc_bs=M * N, nplanes=2, epi=_lib.EPI_BIAS_COL | _lib.EPI_GELU_FWD, bias=cb, d=h, d2=a)
+    hr = planes.double().sum(0) + cb.double()
+    assert rel_err(h.cpu().numpy(), hr.cpu().numpy()) < 1e-6
+    assert rel_err(a.double().cpu().numpy(), torch.nn.functional.gelu(hr).cpu().numpy()) < 8e-3
+    # layer norm over the split axis: moments from the epilogue, apply, backward phases
+    gam, bet = torch.randn(N, device=cuda, generator=g), torch.randn(N, device=cuda, generator=g)
+    u, mr = torch.empty(M, N, device=cuda), torch.empty(M, 2, device=cuda)
+    K.ln_apply(d, st, gam, bet, u, mr, M, N, N, 1e-5)
+    mean = ref.mean(1, keepdim=True)
+    xh = (ref - mean) / torch.sqrt(ref.var(1, unbiased=False, keepdim=True) + 1e-5)
+    assert rel_err(u.cpu().numpy(), (xh * gam.double() + bet.double()).cpu().numpy()) < 1e-4
+    gin = torch.randn(M, N, device=cuda, generator=g)
+    bst = torch.zeros(M, 2, device=cuda)
+    K.ln_bwd_moments(d, gin, gam, mr, bst, M, N)
+    hh = gin.double() * gam.double()
+    assert rel_err(bst[:, 0].cpu().numpy(), hh.sum(1).cpu().numpy()) < 1e-5
+    out, dg, db = torch.empty(M, N, device=cuda), torch.zeros(N, device=cuda), torch.zeros(N, device=cuda)
+    K.ln_bwd_apply(d, gin, gam, mr, bst, resid, out, None, dg, db, M, N, N)
+    rstd = 1 / torch.sqrt(ref.var(1, unbiased=False, keepdim=True) + 1e-5)
+    dx = rstd * (hh - hh.mean(1, keepdim=True) - xh * (hh * xh).mean(1, keepdim=True)) + resid.double()
+    assert rel_err(out.cpu().numpy(), dx.cpu().numpy()) < 1e-4
+    assert rel_err(dg.cpu().numpy(), (gin.double() * xh).sum(0).cpu().numpy()) < 1e-4
+    assert rel_err(db.cpu().numpy(), gin.double().sum(0).cpu().numpy()) < 1e-5

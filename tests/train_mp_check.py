@@ -1,0 +1,83 @@
+"""Multi-GPU captured training step (launched by tests/test_jigsaw_gpu.py under torchrun).
+
+The Jigsaw TrainStep (CUDA graphs, symmetric-memory transport, bf16) with Adam pushing the
+channel-mixing weight panels into the column group's gather slots (jg_adam_push):
+  * after every step each rank's panel slots equal the column group's current bf16 operand
+    tiles, bit for bit (gathered independently over NCCL) — i.e. the next forward reads fresh
+    weights;
+  * an external weight edit (set_param_entry) makes the next call re-gather the panels;
+  * losses and parameters agree with the same run re-gathering panels every forward
+    (JIGSAW_PANEL_PUSH=0) to bf16-step tolerance.
+Prints TRAINMP_OK on success.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+from paper_2507_05753_b200 import Communicator, ModelConfig, MpContext, WeatherMixerModel  # noqa: E402
+from paper_2507_05753_b200.engine import TrainStep  # noqa: E402
+
+CFG = dict(n_vars=72, grid=(32, 64), patch=(2, 2), d_emb=512, d_tok=1024, d_ch=512, n_blocks=3)
+
+
+def panels_fresh(ctx, model, step) -> bool:
+    g = step.ws.grid
+    ok = True
+    for name in g.panel_names:
+        op = model.params[name].op
+        tiles = [torch.empty_like(op) for _ in range(model.R)]
+        dist.all_gather(tiles, op.contiguous(), group=ctx.col_group)
+        ok &= bool(torch.equal(torch.stack(tiles).view(-1), g.panels[name].reshape(-1)))
+    return ok
+
+
+def run(ctx, push: str, x, t):
+    os.environ["JIGSAW_PANEL_PUSH"] = push
+    model = WeatherMixerModel(ctx, ModelConfig(**CFG), seed=0, dtype="bf16")
+    step = TrainStep(model, batch=1, graph=True)
+    losses, fresh = [], []
+    for k in range(4):
+        if k == 2:
+            model.set_param_entry("block1.ch2.w", (3, 5), 0.125)  # external edit -> panels re-gathered
+        losses.append(step(x, t))
+        torch.cuda.synchronize()
+        fresh.append(panels_fresh(ctx, model, step))
+    return model, step, losses, fresh
+
+
+def main():
+    comm = Communicator.from_env()
+    ctx = MpContext(comm, list(range(comm.world_size)))
+    lat, lon = 32, 64 // ctx.R
+    nv = 72 // ctx.C
+    rng = np.random.default_rng(10 + ctx.pos)
+    x = torch.tensor(rng.standard_normal((1, lat, lon, nv)), dtype=torch.float32).pin_memory()
+    t = torch.tensor(rng.standard_normal((1, lat, lon, nv)), dtype=torch.float32).pin_memory()
+    ma, sa, la, fa = run(ctx, "1", x, t)
+    mb, sb, lb, fb = run(ctx, "0", x, t)
+    assert sa._pushing() == (ctx.R > 1) and not sb._pushing(), "push path not taken"
+    assert all(fa), f"rank {comm.rank}: stale panel slots after steps {fa}"
+    assert np.allclose(la, lb, rtol=1e-3), (la, lb)
+    for name, p in ma.params.items():
+        d = (p.data - mb.params[name].data).abs().max().item()
+        s = p.data.abs().max().item() + 1e-12
+        assert d / s < 2e-2, (name, d, s)
+    flag = torch.tensor([1], device="cuda")
+    dist.all_reduce(flag)
+    if comm.rank == 0:
+        print(f"TRAINMP_OK losses {la}", flush=True)
+    dist.barrier()
+    os._exit(0)  # graphs hold NCCL / symmetric-memory state; skip teardown
+
+
+if __name__ == "__main__":
+    main()
