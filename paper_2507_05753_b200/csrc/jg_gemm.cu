@@ -11,8 +11,9 @@
 //   warp 1 lane 0 : MMA issuer — 4 x tcgen05.mma per K-slice into a TMEM accumulator
 //                   (double-buffered: 2 x BN fp32 columns), frees smem via tcgen05.commit.
 //   warp 2        : TMEM allocator.
-//   warps 4..7    : epilogue — tcgen05.ld 32 lanes x 32 columns per step (thread == row),
-//                   applies bias / residual / GELU / GELU' / accumulate / row moments,
+//   warps 4..11   : epilogue — two warps per TMEM lane quarter, each draining alternate
+//                   32-column chunks: tcgen05.ld 32 lanes x 32 columns per step (thread ==
+//                   row), applies bias / residual / GELU / GELU' / accumulate / row moments,
 //                   stores fp32 and/or bf16; releases the TMEM buffer to the MMA warp.
 // Operands may be K-major or MN-major (the NN / NT / TN modes of tensor.py:27-33), are
 // loaded with 3-D TMA (batch as the 3rd dimension) and may be summed over the batch
@@ -24,7 +25,15 @@
 namespace {
 
 constexpr int BM = 128;
-constexpr int NUM_THREADS = 256;
+#ifndef JG_EPI_WARPS
+#define JG_EPI_WARPS 8
+#endif
+#ifndef JG_REG_LO
+#define JG_REG_LO 88
+#define JG_REG_HI 208
+#endif
+constexpr int NUM_EPI_WARPS = JG_EPI_WARPS;  // 8: two per TMEM lane quarter, splitting a tile's column chunks
+constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
 constexpr int SMEM_BUDGET = 196 * 1024;
 
 struct GemmParams {
@@ -71,7 +80,7 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET / STAGE_BYTES) > 8 ? 8 : (SMEM_BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;          // double-buffered fp32 accumulator
-  static constexpr int EPI_STAGE_BYTES = 4 * 4096;  // one 32x32 fp32 staging tile per epilogue warp
+  static constexpr int EPI_STAGE_BYTES = NUM_EPI_WARPS * 4096;  // one 32x32 fp32 staging tile per epilogue warp
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t IDESC_BASE =
       (1u << 4)                                    // D format: f32
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     }
     for (int s = 0; s < 2; ++s) {
       jgd::mbar_init(&tfull[s], 1);
-      jgd::mbar_init(&tempty[s], 4 * CG);  // every epilogue warp of the pair drains the leader's slot
+      jgd::mbar_init(&tempty[s], NUM_EPI_WARPS * CG);  // every epilogue warp of the pair drains the leader's slot
     }
     jgd::mbar_fence_init();
   }
@@ -180,6 +189,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   const int kb_per_tile = p.nseg * kb_batches * p.num_kb;
   const int tiles_per_batch = p.m_tiles * p.n_tiles;
 
+  // register split: warpgroup 0 (TMA producer, MMA issuer, TMEM allocator) needs few; the two
+  // epilogue warpgroups get the rest (128 x 88 + 256 x 208 <= 64K; 40 / 232 and no split measured slower at locked clocks)
+#define JG_STR2(x) #x
+#define JG_STR(x) JG_STR2(x)
+  if (warp < 4) {
+#if JG_REG_LO > 0
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 " JG_STR(JG_REG_LO) ";\n" ::: "memory");
+#endif
   if (warp == 0 && lane == 0) {
     // ===================== TMA producer =====================
     int stage = 0;
@@ -269,9 +286,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
         jgd::umma_commit(&tfull[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+#if JG_REG_LO > 0
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 " JG_STR(JG_REG_HI) ";\n" ::: "memory");
+#endif
     // ===================== epilogue =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;             // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;   // which alternate 32-column chunks of the tile it drains
+    constexpr int CSTEP = NUM_EPI_WARPS / 4;
     uint8_t* stg = smem_epi + (warp - 4) * 4096;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -310,7 +333,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       float s1 = 0.f, s2 = 0.f;
 
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += CSTEP) {
         const int col0 = n0 + c * 32;
         if (col0 >= p.n) break;  // warp-uniform
         float v[32];
