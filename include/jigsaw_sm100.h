@@ -114,6 +114,25 @@ typedef struct jg_gemm_desc {
   void* d_planes[8];
   /* extra destinations of D and D2 (TMA-store epilogue only; same ld / batch stride) */
   jg_bcast d_bcast, d2_bcast;
+  /* Fused Jigsaw reduce-scatter over peer memory (replaces the partial-sum exchange of
+   * pnt/pnn/ptn, parallel.py:118-132, 200-215, 287-300, and the sum + ShardedLinear tail that
+   * follows it, parallel.py:521-525). Batch b of the GEMM is the partial product owned by group
+   * member b; the d_planes[b] != NULL batches are stored raw (dtype rs_part_type, row stride ldd)
+   * into their owners' buffers, and after a tile's stores have landed the epilogue adds 1
+   * (system-scope release) to rs_flag_peers[b][flag(tile)]. With rs_flags != NULL, rs_own names
+   * this rank's own batch (rs_flags == NULL: no own batch, rs_own ignored; a zeroed descriptor
+   * disables the whole mode): its tiles run after every remote tile, each waits until rs_flags[flag(tile)] reaches
+   * rs_need (one arrival per peer), then the epilogue forms sum_{j < rs_nsrc} plane_j in order —
+   * plane rs_src_idx being this rank's accumulator rounded to rs_part_type, the others read from
+   * rs_src + j * rs_src_stride (row stride ldd) — and applies the regular epilogue to it exactly
+   * as jg_epilogue would (alpha, bias, residual, GELU, moments, D / D2 / broadcast stores; the
+   * batch strides are ignored: batch 0 addressing). Flag counters are returned to zero by the
+   * consumer. flag(tile) = (tile_in_batch * cta_group + cta_rank) * 8 + epilogue_warp, below
+   * rs_flag_cap. */
+  uint32_t* rs_flags;
+  uint32_t* rs_flag_peers[8];
+  const void* rs_src; int64_t rs_src_stride;
+  int32_t rs_part_type, rs_nsrc, rs_src_idx, rs_own, rs_need, rs_flag_cap;
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);

@@ -112,6 +112,10 @@ class GemmDesc(ctypes.Structure):
         ("adam_beta2", ctypes.c_float), ("adam_eps", ctypes.c_float),
         ("d_planes", ctypes.c_void_p * 8),
         ("d_bcast", Bcast), ("d2_bcast", Bcast),
+        ("rs_flags", ctypes.c_void_p), ("rs_flag_peers", ctypes.c_void_p * 8),
+        ("rs_src", ctypes.c_void_p), ("rs_src_stride", ctypes.c_int64),
+        ("rs_part_type", ctypes.c_int32), ("rs_nsrc", ctypes.c_int32), ("rs_src_idx", ctypes.c_int32),
+        ("rs_own", ctypes.c_int32), ("rs_need", ctypes.c_int32), ("rs_flag_cap", ctypes.c_int32),
     ]
 
 

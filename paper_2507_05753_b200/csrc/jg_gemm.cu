@@ -66,8 +66,117 @@ struct GemmParams {
   float* adam_m; float* adam_v; __nv_bfloat16* adam_pbf16; const int32_t* adam_step;
   float adam_lr, adam_b1, adam_b2, adam_eps;
   void* d_planes[8];
-  int remote;
+  int remote;              // some output goes to a peer: system-scope fence at the end
+  int planes;              // d_planes in use: per-batch D store maps
+  // fused reduce-scatter (jg_gemm_desc rs_*): raw partial tiles to the owners + arrival flags,
+  // own-plane tiles last, summed with the peers' partials in this rank's buffer
+  int rs_mode;
+  int dmap_bf16[8];        // dtype of tma_d[b]
+  uint32_t* rs_flags;
+  uint32_t* rs_flag_peers[8];
+  const void* rs_src; int64_t rs_src_stride;
+  int rs_part_bf16, rs_nsrc, rs_src_idx, rs_own, rs_need;
+  // wave schedule of a fused reduce-scatter with an own plane: the persistent loop's positions
+  // come in waves of `units` tiles (one per CTA unit); wave k holds own-plane tiles
+  // wave_idx[k]*units.. (wave_kind 1) or remote-partial tiles (0). Own waves alternate with
+  // remote waves (after a head of remote waves), so each CTA alternates the heavy own epilogue
+  // (peer partial loads, residual, two outputs) with light raw partial stores, and an own tile
+  // always follows its peers' partials by at least one wave. nwaves == 0: linear order.
+  int num_pos, units, nwaves;
+  uint8_t wave_kind[64], wave_idx[64];
+  int rs_dbg;              // JG_RS_DBG ablations (timing only, results wrong): 1 no fences, 2 no own wait, 4 no peer loads
 };
+
+// Fused reduce-scatter: the own plane's tiles run after every remote tile (logical batch order
+// own+1, own+2, ..., own), so each rank first feeds its peers, then consumes what they fed it.
+template <bool RS>
+__device__ __forceinline__ int rs_batch(const GemmParams& p, int lb) {
+  return (RS && p.rs_own >= 0) ? (p.rs_own + 1 + lb) % p.batch : lb;
+}
+
+// position of the persistent tile loop -> (output batch, tile within the batch); false: a hole
+template <bool RS>
+__device__ __forceinline__ bool tile_at(const GemmParams& p, int pos, int tiles_per_batch, int& tb, int& rem) {
+  if (!RS || p.nwaves == 0) {
+    const int lb = p.reduce_batch ? 0 : pos / tiles_per_batch;
+    rem = pos - lb * tiles_per_batch;
+    tb = p.reduce_batch ? 0 : rs_batch<RS>(p, lb);
+    return true;
+  }
+  const int k = pos / p.units;
+  const int t = p.wave_idx[k] * p.units + (pos - k * p.units);
+  if (p.wave_kind[k]) {
+    tb = p.rs_own;
+    rem = t;
+    return t < tiles_per_batch;
+  }
+  const int nr = p.batch - 1;
+  if (t >= nr * tiles_per_batch) return false;
+  rem = t / nr;
+  const int b = t - rem * nr;
+  tb = b < p.rs_own ? b : b + 1;
+  return true;
+}
+
+__device__ __forceinline__ void rs_wait_flag(const uint32_t* f, uint32_t need) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v >= need) break;
+    __nanosleep(64);
+    if (clock64() - t0 > (1ll << 33)) __trap();  // a peer never arrived (~4 s): fail loudly, never hang
+  }
+}
+
+__device__ __forceinline__ void rs_add_flag(uint32_t* f, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+
+// wait until at most n of this thread's most recent bulk async-groups are still pending
+__device__ __forceinline__ void bulk_wait_le(int n) {
+  switch (n) {
+    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+  }
+}
+
+// Arrival of a partial tile at its owner, signalled lazily: the tile's stores are left in flight
+// while the warp drains the next tile, whose own store groups (`newer`) may stay pending.
+__device__ __forceinline__ void rs_signal(uint32_t*& pend, int newer, int lane, int dbg) {
+  if (pend == nullptr) return;
+  if (lane == 0) {
+    if (!(dbg & 1)) {
+      bulk_wait_le(newer);  // the tile's stores are complete ...
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }                       // ... and ordered before the release below
+    rs_add_flag(pend, 1u);
+  }
+  __syncwarp();
+  pend = nullptr;
+}
+
+// 8 contiguous partial-product elements written by a peer during this kernel (L2, not L1)
+__device__ __forceinline__ void load8_cg(const void* base, int64_t off, bool bf16, float* v) {
+  if (bf16) {
+    const uint4 raw = __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + off));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  } else {
+    const float4* q = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + off);
+    const float4 a = __ldcg(q), b = __ldcg(q + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
 
 template <int BN, bool TF32, int CG = 1>
 struct Cfg {
@@ -135,7 +244,7 @@ __device__ __forceinline__ void tile_coords(int rem, int m_tiles, int n_tiles, i
   ni = r / gm;
 }
 
-template <int BN, bool TF32, int CG>
+template <int BN, bool TF32, int CG, bool RS>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
   using C = Cfg<BN, TF32, CG>;
   static_assert(CG == 1 || !TF32, "2-CTA path is bf16 only");
@@ -201,9 +310,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     // ===================== TMA producer =====================
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
-      const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
-      const int rem = tile - tb * tiles_per_batch;
+    for (int tile = tile0; tile < p.num_pos; tile += tstep) {
+      int tb, rem;
+      if (!tile_at<RS>(p, tile, tiles_per_batch, tb, rem)) continue;
       int mi, ni;
       tile_coords(rem, p.m_tiles, p.n_tiles, mi, ni);
       const int m0 = mi * (BM * CG) + BM * static_cast<int>(cta_rank);
@@ -254,7 +363,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+    for (int tile = tile0; tile < p.num_pos; tile += tstep) {
+      int tb_, rem_;
+      if (!tile_at<RS>(p, tile, tiles_per_batch, tb_, rem_)) continue;
       jgd::mbar_wait(&tempty[acc], acc_phase ^ 1);
       jgd::tc_fence_after();
       const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -306,17 +417,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       bc1 = 1.0f / (1.0f - powf(ab1, (float)t));
       bc2 = 1.0f / (1.0f - powf(ab2, (float)t));
     }
-    for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
-      const int tb = p.reduce_batch ? 0 : tile / tiles_per_batch;
-      const int rem = tile - tb * tiles_per_batch;
+    uint32_t* pend = nullptr;  // flag of the last partial tile whose arrival is not yet signalled
+    for (int tile = tile0; tile < p.num_pos; tile += tstep) {
+      int tb, rem;
+      if (!tile_at<RS>(p, tile, tiles_per_batch, tb, rem)) continue;
       int mi, ni;
       tile_coords(rem, p.m_tiles, p.n_tiles, mi, ni);
       const int m0 = mi * (BM * CG) + BM * static_cast<int>(cta_rank);
       const int n0 = ni * BN;
+      int ngroups = 0;  // bulk store groups this warp commits for this tile
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < p.m;
+      // fused reduce-scatter roles of this tile: own plane (sum + full epilogue) or a raw
+      // partial for its owner (no epilogue); eb = batch index of the epilogue operands
+      const bool own = RS && p.rs_mode && tb == p.rs_own;
+      const bool part = RS && p.rs_mode && !own;
+      const uint32_t tepi = part ? 0u : epi;
+      const int eb = (RS && p.rs_mode) ? 0 : tb;
+      const int fidx = (rem * CG + static_cast<int>(cta_rank)) * NUM_EPI_WARPS + (warp - 4);
       jgd::mbar_wait(&tfull[acc], acc_phase);
       jgd::tc_fence_after();
+      if (RS && own) {
+        rs_signal(pend, 0, lane, p.rs_dbg);  // peers may be waiting for it: never hold it across a wait
+        if (!(p.rs_dbg & 2)) rs_wait_flag(p.rs_flags + fidx, static_cast<uint32_t>(p.rs_need));
+        __syncwarp();
+        if (lane == 0) rs_add_flag(p.rs_flags + fidx, static_cast<uint32_t>(-p.rs_need));  // re-arm for reuse
+      }
 
       // per-batch destination (fused reduce-scatter into a peer's buffer) or the regular strided D
       void* dbase = p.d;
@@ -325,11 +451,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
         dbase = p.d_planes[tb];
         drow = static_cast<int64_t>(row) * p.ldd;
       }
-      const int64_t d2row = tb * p.d2_bs + static_cast<int64_t>(row) * p.ldd2;
-      const int64_t rrow = tb * p.r_bs + static_cast<int64_t>(row) * p.ldr;
-      const int64_t prow = tb * p.p_bs + static_cast<int64_t>(row) * p.ldp;
+      const int64_t d2row = eb * p.d2_bs + static_cast<int64_t>(row) * p.ldd2;
+      const int64_t rrow = eb * p.r_bs + static_cast<int64_t>(row) * p.ldr;
+      const int64_t prow = eb * p.p_bs + static_cast<int64_t>(row) * p.ldp;
       float rbias = 0.f;
-      if ((epi & JG_EPI_BIAS_ROW) && row_ok) rbias = p.bias[tb * p.bias_bs + row];
+      if ((tepi & JG_EPI_BIAS_ROW) && row_ok) rbias = p.bias[eb * p.bias_bs + row];
       float s1 = 0.f, s2 = 0.f;
 
 #pragma unroll 1
@@ -340,7 +466,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
         jgd::tmem_ld32(tmem_base + static_cast<uint32_t>(acc * BN + c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
         const bool full_chunk = col0 + 32 <= p.n;
         const int ncol = full_chunk ? 32 : p.n - col0;
-        if (row_ok) {
+        if (own && row_ok) {
+          // sum of the group's partial planes in member order (exactly jg_epilogue's sum of the
+          // reduce-scattered planes: this rank's own plane rounded to the partial dtype), then
+          // the epilogue in jg_epilogue's order: alpha, row bias, column bias, residual, GELU'
+          float s[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) s[j] = 0.f;
+          const int64_t srow = static_cast<int64_t>(row) * p.ldd + col0;
+          for (int src = 0; src < p.rs_nsrc; ++src) {
+            if (src == p.rs_src_idx || (p.rs_dbg & 4)) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) s[j] += p.rs_part_bf16 ? __bfloat162float(__float2bfloat16_rn(v[j])) : v[j];
+            } else if (full_chunk) {
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                float t[8];
+                load8_cg(p.rs_src, src * p.rs_src_stride + srow + g * 8, p.rs_part_bf16, t);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s[g * 8 + j] += t[j];
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < ncol) s[j] += jgd::load1(p.rs_src, src * p.rs_src_stride + srow + j, p.rs_part_bf16);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = s[j] * p.alpha + rbias;
+          if (epi & JG_EPI_BIAS_COL) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (j < ncol) ? __ldg(p.bias + col0 + j) : 0.f;
+          }
+        }
+        if (row_ok && !own && !part) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
         if (epi & JG_EPI_BIAS_COL) {
@@ -352,6 +511,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] += rbias;
         }
+        }  // regular (non-reduce-scatter) alpha / bias
+        if (row_ok && !part) {
         if (epi & JG_EPI_RESID) {
           if (full_chunk) {
 #pragma unroll
@@ -476,15 +637,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
         if (p.tma_store) {
           // stage the warp's 32 x 32 chunk in swizzled smem, one TMA bulk tensor store per output
           const int rbase = m0 + q * 32;
-          if (p.remote || p.d != nullptr)
-            stage_store(stg, v, p.d_bf16, lane, &p.tma_d[p.remote ? tb : 0], col0, rbase, p.remote ? 0 : tb,
-                        p.tma_dx, p.nb_d);
+          if (part) {
+            stage_store(stg, v, p.dmap_bf16[tb], lane, &p.tma_d[tb], col0, rbase, 0);
+            ++ngroups;
+            continue;
+          }
+          const bool per_batch_map = p.planes || (RS && p.rs_mode);
+          if (per_batch_map || p.d != nullptr)
+            stage_store(stg, v, p.dmap_bf16[per_batch_map ? tb : 0], lane, &p.tma_d[per_batch_map ? tb : 0], col0,
+                        rbase, per_batch_map ? 0 : tb, p.tma_dx, p.nb_d);
           if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
             if (epi & JG_EPI_GELU_FWD) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = jgd::gelu_f(v[j]);
             }
-            stage_store(stg, v, p.d2_bf16, lane, &p.tma_d2, col0, rbase, tb, p.tma_d2x, p.nb_d2);
+            stage_store(stg, v, p.d2_bf16, lane, &p.tma_d2, col0, rbase, eb, p.tma_d2x, p.nb_d2);
           }
           continue;
         }
@@ -514,10 +681,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           }
         }
       }
-      if ((epi & JG_EPI_STATS) && row_ok) {
-        float* sp = p.stats + tb * p.stats_bs + static_cast<int64_t>(row) * 2;
+      if ((tepi & JG_EPI_STATS) && row_ok) {
+        float* sp = p.stats + eb * p.stats_bs + static_cast<int64_t>(row) * 2;
         atomicAdd(sp, s1);
         atomicAdd(sp + 1, s2);
+      }
+      if (RS && part && p.rs_flag_peers[tb] != nullptr) {
+        // the previous partial tile's stores are older than this tile's ngroups: signal it now,
+        // this one after the next tile (or before any own-tile wait / at the end)
+        rs_signal(pend, ngroups, lane, p.rs_dbg);
+        pend = p.rs_flag_peers[tb] + fidx;
       }
       jgd::tc_fence_before();
       __syncwarp();
@@ -529,6 +702,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if constexpr (RS) rs_signal(pend, 0, lane, p.rs_dbg);
     if (lane == 0) jgd::bulk_wait0();  // every TMA store of this warp has landed
     __syncwarp();
     if (p.remote) __threadfence_system();  // peer stores visible before the group barrier
@@ -631,20 +805,18 @@ int make_store_map(CUtensorMap* map, void* ptr, bool bf16, int64_t rows, int64_t
   return JG_OK;
 }
 
-template <int BN, bool TF32, int CG>
+template <int BN, bool TF32, int CG, bool RS = false>
 int launch(GemmParams& p, cudaStream_t stream) {
   using C = Cfg<BN, TF32, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, TF32, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, TF32, CG, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return jg::cuda_check(attr_err, "cudaFuncSetAttribute(gemm)");
-  const int max_units = jg::num_sms() / CG;
-  const int units = p.num_tiles < max_units ? p.num_tiles : max_units;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(units * CG);
+  cfg.gridDim = dim3(p.units * CG);
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
@@ -655,7 +827,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, TF32, CG>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, TF32, CG, RS>, p);
   if (e != cudaSuccess) return jg::cuda_check(e, "gemm_kernel launch");
   JG_LAUNCH_CHECK("gemm_kernel");
   return JG_OK;
@@ -740,6 +912,12 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   const int64_t nt = static_cast<int64_t>(p.m_tiles) * p.n_tiles * out_batches;
   JG_SHAPE_CHECK(nt < (1ll << 31), "jg_gemm: too many tiles");
   p.num_tiles = static_cast<int>(nt);
+  p.num_pos = p.num_tiles;
+  {
+    const int max_units = jg::num_sms() / cg;
+    p.units = p.num_tiles < max_units ? p.num_tiles : max_units;
+  }
+  p.nwaves = 0;
 
   p.nseg = tf32 ? 3 : 1;
   const void* as[3] = {g->a, g->a, g->a_lo};
@@ -768,36 +946,104 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   for (int i = 0; i < 8; ++i) {
     p.d_planes[i] = g->d_planes[i];
     if (g->d_planes[i] != nullptr) p.remote = 1;
+    p.rs_flag_peers[i] = g->rs_flag_peers[i];
   }
+  p.planes = p.remote;
+  const bool rs_has_own = g->rs_flags != nullptr;  // rs_own is meaningful only with a flag array
+  p.rs_own = rs_has_own ? g->rs_own : -1;
+  p.rs_mode = rs_has_own ? 1 : 0;
+  for (int i = 0; i < 8; ++i)
+    if (g->rs_flag_peers[i] != nullptr) p.rs_mode = 1;
   JG_SHAPE_CHECK(!p.remote || (!g->reduce_batch && g->batch <= 8 && !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM))),
                  "jg_gemm: d_planes needs <= 8 independent output batches and no ACCUM/ADAM");
+  if (p.rs_mode) {
+    JG_SHAPE_CHECK(!g->reduce_batch && g->batch <= 8 && p.rs_own >= -1 && p.rs_own < g->batch && !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM)),
+                   "jg_gemm: fused reduce-scatter needs <= 8 independent output batches and no ACCUM/ADAM");
+    JG_SHAPE_CHECK(NUM_EPI_WARPS == 8 && static_cast<int64_t>(p.m_tiles) * p.n_tiles * cg * NUM_EPI_WARPS <= g->rs_flag_cap,
+                   "jg_gemm: fused reduce-scatter flag array too small (%lld tiles, cap %d)",
+                   (long long)p.m_tiles * p.n_tiles, g->rs_flag_cap);
+    JG_SHAPE_CHECK(g->rs_part_type == JG_BF16 || g->rs_part_type == JG_F32, "jg_gemm: rs_part_type must be f32 or bf16");
+    for (int b = 0; b < static_cast<int>(g->batch); ++b) {
+      const bool own = b == p.rs_own;
+      JG_SHAPE_CHECK(own ? g->d_planes[b] == nullptr : (g->d_planes[b] != nullptr && g->rs_flag_peers[b] != nullptr),
+                     "jg_gemm: fused reduce-scatter batch %d needs %s", b,
+                     own ? "no d_planes entry (own plane)" : "a d_planes entry and a peer flag array");
+    }
+    if (p.rs_own >= 0)
+      JG_SHAPE_CHECK(g->d != nullptr && g->rs_src != nullptr && g->rs_nsrc >= 1 &&
+                         g->rs_nsrc <= 8 && g->rs_src_idx >= 0 && g->rs_src_idx < g->rs_nsrc && g->rs_need >= 0 &&
+                         aligned16(g->rs_src) && (g->rs_src_stride * (g->rs_part_type == JG_BF16 ? 2 : 4)) % 16 == 0,
+                     "jg_gemm: fused reduce-scatter own plane needs D, flags and an aligned partial-plane source");
+  }
+  p.rs_flags = g->rs_flags;
+  p.rs_src = g->rs_src;
+  p.rs_src_stride = g->rs_src_stride;
+  p.rs_part_bf16 = g->rs_part_type == JG_BF16;
+  p.rs_nsrc = g->rs_nsrc;
+  p.rs_src_idx = g->rs_src_idx;
+  p.rs_need = g->rs_need;
+  static const int rs_dbg = getenv("JG_RS_DBG") ? atoi(getenv("JG_RS_DBG")) : 0;
+  p.rs_dbg = rs_dbg;
+  static const bool rs_linear = getenv("JG_RS_LINEAR") != nullptr;
+  if (p.rs_own >= 0 && p.batch >= 2 && !rs_linear) {
+    // head of nr + 1 remote waves, then (own wave, nr remote waves) cycles; leftovers at the end
+    const int64_t T = static_cast<int64_t>(p.m_tiles) * p.n_tiles, U = p.units, nr = p.batch - 1;
+    const int64_t wo = (T + U - 1) / U, wr = (nr * T + U - 1) / U;
+    if (wo + wr <= 64) {
+      int64_t io = 0, ir = 0, w = 0;
+      auto push = [&](int kind, int64_t idx) {
+        p.wave_kind[w] = static_cast<uint8_t>(kind);
+        p.wave_idx[w] = static_cast<uint8_t>(idx);
+        ++w;
+      };
+      for (; ir < wr && ir < nr + 1; ++ir) push(0, ir);
+      while (io < wo || ir < wr) {
+        if (io < wo) push(1, io++);
+        for (int64_t j = 0; j < nr && ir < wr; ++j) push(0, ir++);
+      }
+      p.nwaves = static_cast<int>(w);
+      p.num_pos = static_cast<int>(w * U);
+    }
+  }
   // TMA-store epilogue whenever D is write-only (no read-modify-write of D)
   p.tma_store = !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM)) && (g->d != nullptr || p.remote);
+  JG_SHAPE_CHECK(!p.rs_mode || p.tma_store, "jg_gemm: fused reduce-scatter needs the TMA-store epilogue");
   if (p.tma_store) {
     const bool dbf = g->d_type == JG_BF16;
-    if (p.remote) {
+    // per-output-batch maps (d_planes / fused reduce-scatter) address one plane each (batch 0)
+    const int64_t eb_batches = p.rs_mode ? 1 : out_batches;
+    if (p.rs_mode) {
       for (int b = 0; b < static_cast<int>(out_batches); ++b) {
+        const bool own = b == p.rs_own;
+        p.dmap_bf16[b] = own ? dbf : p.rs_part_bf16;
+        int rc = make_store_map(&p.tma_d[b], own ? g->d : g->d_planes[b], p.dmap_bf16[b], g->m, g->n, g->ldd, 0, 1);
+        if (rc) return rc;
+      }
+    } else if (p.remote) {
+      for (int b = 0; b < static_cast<int>(out_batches); ++b) {
+        p.dmap_bf16[b] = dbf;
         int rc = make_store_map(&p.tma_d[b], g->d_planes[b] ? g->d_planes[b] : g->d, dbf, g->m, g->n, g->ldd, 0, 1);
         if (rc) return rc;
       }
     } else {
+      p.dmap_bf16[0] = dbf;
       int rc = make_store_map(&p.tma_d[0], g->d, dbf, g->m, g->n, g->ldd, g->d_bstride, out_batches);
       if (rc) return rc;
     }
     if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
-      int rc = make_store_map(&p.tma_d2, g->d2, g->d2_type == JG_BF16, g->m, g->n, g->ldd2, g->d2_bstride, out_batches);
+      int rc = make_store_map(&p.tma_d2, g->d2, g->d2_type == JG_BF16, g->m, g->n, g->ldd2, g->d2_bstride, eb_batches);
       if (rc) return rc;
     }
-    p.nb_d = p.remote ? 0 : g->d_bcast.n;
+    p.nb_d = (p.remote && !p.rs_mode) ? 0 : g->d_bcast.n;
     p.nb_d2 = (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) ? g->d2_bcast.n : 0;
     JG_SHAPE_CHECK(p.nb_d >= 0 && p.nb_d <= 4 && p.nb_d2 >= 0 && p.nb_d2 <= 4, "jg_gemm: at most 4 broadcast targets");
     for (int i = 0; i < p.nb_d; ++i) {
-      int rc = make_store_map(&p.tma_dx[i], g->d_bcast.ptr[i], dbf, g->m, g->n, g->ldd, g->d_bstride, out_batches);
+      int rc = make_store_map(&p.tma_dx[i], g->d_bcast.ptr[i], dbf, g->m, g->n, g->ldd, g->d_bstride, eb_batches);
       if (rc) return rc;
     }
     for (int i = 0; i < p.nb_d2; ++i) {
       int rc = make_store_map(&p.tma_d2x[i], g->d2_bcast.ptr[i], g->d2_type == JG_BF16, g->m, g->n, g->ldd2,
-                              g->d2_bstride, out_batches);
+                              g->d2_bstride, eb_batches);
       if (rc) return rc;
     }
   } else {
@@ -805,10 +1051,20 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   }
   if (p.nb_d || p.nb_d2) p.remote = 1;  // system fence at the end: peers read after the barrier
 
+  JG_SHAPE_CHECK(!(tf32 && p.rs_mode), "jg_gemm: fused reduce-scatter is bf16 only");
   if (tf32) {
     if (bn == 256) return launch<256, true, 1>(p, stream);
     if (bn == 128) return launch<128, true, 1>(p, stream);
     return launch<64, true, 1>(p, stream);
+  }
+  if (p.rs_mode) {  // fused reduce-scatter variant (bf16 only; rs code compiled out of the others)
+    if (cg == 2) {
+      if (bn == 256) return launch<256, false, 2, true>(p, stream);
+      return launch<128, false, 2, true>(p, stream);
+    }
+    if (bn == 256) return launch<256, false, 1, true>(p, stream);
+    if (bn == 128) return launch<128, false, 1, true>(p, stream);
+    return launch<64, false, 1, true>(p, stream);
   }
   if (cg == 2) {
     if (bn == 256) return launch<256, false, 2>(p, stream);

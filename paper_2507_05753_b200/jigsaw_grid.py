@@ -39,7 +39,7 @@ import torch
 
 from . import _lib
 from . import kernels as K
-from .transport import NcclTransport, SymmTransport
+from .transport import NcclTransport, SymmTransport, fused_rs_enabled
 
 KM, MN = _lib.JG_KMAJOR, _lib.JG_MNMAJOR
 E_ACC, E_BCOL, E_BROW, E_RES = _lib.EPI_ACCUM, _lib.EPI_BIAS_COL, _lib.EPI_BIAS_ROW, _lib.EPI_RESID
@@ -94,6 +94,8 @@ class GridWorkspace:
                     for name, shape, dt in spec:
                         tr.reserve(name, shape, dt)
         self.kind = kind
+        # GEMM + reduce-scatter + epilogue in one kernel (symmetric-memory transport)
+        self.fused = kind == "symm" and fused_rs_enabled()
         # reduce-scatter partial planes travel in the operand dtype (bf16 mode: half the NVLink bytes
         # and half the epilogue reads; summed in fp32); JIGSAW_PARTIALS=fp32 keeps fp32 partials
         bf = od == torch.bfloat16 and os.environ.get("JIGSAW_PARTIALS", "bf16") != "fp32"
@@ -166,9 +168,12 @@ def chan_fwd(m, g, X, panel, M, kin_l, nout, **epi):
     C = m.C
     nl = nout // C
 
-    def fn(s, D, d_bs, dpl):
-        K.gemm(D, X, panel, KM, KM, M, nl, kin_l, C, 0, nl * kin_l, d_bs=d_bs, d_planes=dpl)
+    def fn(s, D, d_bs, dpl, **kw):
+        K.gemm(D, X, panel, KM, KM, M, nl, kin_l, C, 0, nl * kin_l, d_bs=d_bs, d_planes=dpl, **kw)
 
+    if g.fused:
+        g.row.rs_gemm_fused(M, nl, g.pdt, fn, **epi)
+        return
     acc, npl, ps = g.row.rs_gemm(M, nl, g.pdt, fn)
     K.epilogue(acc, M, nl, acc_bs=ps, nplanes=npl, **epi)
 
@@ -189,12 +194,15 @@ def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None
     else:
         q, nr = g.q, nout // R
 
-        def fn(s, D, d_bs, dpl):  # rows sub-chunk s of every gathered plane j -> owner j*q+s
+        def fn(s, D, d_bs, dpl, **kw):  # rows sub-chunk s of every gathered plane j -> owner j*q+s
             K.gemm(D, dyrow[..., s * nr:], X, MN, MN, nr, kin_l, M, C, M * nl, 0, d_bs=d_bs, d_planes=dpl,
-                   lda=nl)
+                   lda=nl, **kw)
 
-        acc, npl, ps = g.col.rs_gemm(nr, kin_l, g.pdt, fn, q=q)
-        _wgrad_planes(m, g, wname, acc, npl, ps, nr * kin_l)
+        if g.fused and getattr(m, "_grad_overwrite", False) and getattr(m, "_fused_adam", None) is None:
+            g.col.rs_gemm_fused(nr, kin_l, g.pdt, fn, q=q, d=m.params[wname].grad)  # straight into the gradient
+        else:
+            acc, npl, ps = g.col.rs_gemm(nr, kin_l, g.pdt, fn, q=q)
+            _wgrad_planes(m, g, wname, acc, npl, ps, nr * kin_l)
     K.colsum(bias_src, m.params[bname].grad, M, nl)
 
 
@@ -212,14 +220,17 @@ def tok1_fwd(m, g, ws, j, bi, b, urow):
         return ws.a[j][bi]
     q = g.q
 
-    def fn(s, D, d_bs, dpl):  # rows [s*Er, (s+1)*Er) of plane j -> owner j*q+s
+    def fn(s, D, d_bs, dpl, **kw):  # rows [s*Er, (s+1)*Er) of plane j -> owner j*q+s
         K.gemm(D, urow[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
-               d_planes=dpl, lda=El)
+               d_planes=dpl, lda=El, **kw)
 
-    acc, npl, pst = g.col.rs_gemm(Er, Kl, g.pdt, fn, q=q)
     ha = g.col.dest((Er, Kl), m.op_dtype, slot=f"a_col{j}", sub=bi, nsub=B)   # gelu(h) pushed to peers
-    K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data,
-               d=ws.h[j][bi], d2=ha.own, d2_bcast=ha.peers)
+    epi = dict(epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d=ws.h[j][bi], d2=ha.own, d2_bcast=ha.peers)
+    if g.fused:
+        g.col.rs_gemm_fused(Er, Kl, g.pdt, fn, q=q, **epi)
+    else:
+        acc, npl, pst = g.col.rs_gemm(Er, Kl, g.pdt, fn, q=q)
+        K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, **epi)
     g.col.publish(ha)
     return ha.planes.view(-1, Kl)
 
@@ -229,12 +240,16 @@ def tok2_fwd(m, g, ws, j, bi, b, acol):
     p, C = m.params, m.C
     Tl, El, Kl = ws.Tl, ws.El, ws.Kl
 
-    def fn(s, D, d_bs, dpl):
-        K.gemm(D, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
+    def fn(s, D, d_bs, dpl, **kw):
+        K.gemm(D, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
 
+    epi = dict(epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data, resid=ws.res[j][bi], d=ws.x2[j][bi],
+               stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
+    if g.fused:
+        g.row.rs_gemm_fused(Tl, El, g.pdt, fn, **epi)
+        return
     acc, npl, ps = g.row.rs_gemm(Tl, El, g.pdt, fn)
-    K.epilogue(acc, Tl, El, acc_bs=ps, nplanes=npl, epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data,
-               resid=ws.res[j][bi], d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
+    K.epilogue(acc, Tl, El, acc_bs=ps, nplanes=npl, **epi)
 
 
 def tok2_bwd(m, g, ws, j, bi, b, grow, acol):
@@ -251,13 +266,17 @@ def tok2_bwd(m, g, ws, j, bi, b, grow, acol):
     else:
         q = g.q
 
-        def fn(s, D, d_bs, dpl):
+        def fn(s, D, d_bs, dpl, **kw):
             K.gemm(D, grow[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
-                   d_planes=dpl, lda=El)
+                   d_planes=dpl, lda=El, **kw)
 
-        acc, npl, pst = g.col.rs_gemm(Er, Kl, g.pdt, fn, q=q)
         hg = g.col.dest((Er, Kl), m.op_dtype, slot="gh_col", sub=bi, nsub=B)
-        K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_GB, pre=ws.h[j][bi], d=hg.own, d_bcast=hg.peers)
+        epi = dict(epi=E_GB, pre=ws.h[j][bi], d=hg.own, d_bcast=hg.peers)
+        if g.fused:
+            g.col.rs_gemm_fused(Er, Kl, g.pdt, fn, q=q, **epi)
+        else:
+            acc, npl, pst = g.col.rs_gemm(Er, Kl, g.pdt, fn, q=q)
+            K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, **epi)
         g.col.publish(hg)
         gh_local, ghcol = hg.own, hg.planes.view(-1, Kl)
     K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
@@ -273,12 +292,15 @@ def tok1_bwd(m, g, ws, j, bi, b, ghcol):
     p, C = m.params, m.C
     Tl, El, Kl, B = ws.Tl, ws.El, ws.Kl, ws.B
 
-    def fn(s, D, d_bs, dpl):
-        K.gemm(D, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl)
+    def fn(s, D, d_bs, dpl, **kw):
+        K.gemm(D, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
 
-    acc, npl, ps = g.row.rs_gemm(Tl, El, g.pdt, fn, out=ws.gu[bi])
-    if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
-        K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
+    if g.fused:
+        g.row.rs_gemm_fused(Tl, El, g.pdt, fn, d=ws.gu[bi])
+    else:
+        acc, npl, ps = g.row.rs_gemm(Tl, El, g.pdt, fn, out=ws.gu[bi])
+        if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
+            K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
     urow = g.row.persistent(f"u_row{j}").view(C, B, Tl, El)[:, bi]
     out, kw = m._wgrad(b + "tok1.w") if bi == 0 or B == 1 else (p[b + "tok1.w"].grad, {"epi": E_ACC})
     if bi == 0 and B > 1 and kw.get("epi") == _lib.EPI_ADAM:

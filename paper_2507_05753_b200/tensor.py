@@ -83,7 +83,7 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
               stats_bs: int = 0, d_bs: int | None = None, d2_bs: int | None = None,
               lda: int | None = None, ldb: int | None = None, ldd: int | None = None,
               a_lo: torch.Tensor | None = None, b_lo: torch.Tensor | None = None, adam=None,
-              d_planes=None, d_bcast=None, d2_bcast=None) -> torch.Tensor:
+              d_planes=None, d_bcast=None, d2_bcast=None, rs: dict | None = None) -> torch.Tensor:
     """Low-level fused GEMM: out[b] (op)= sum_k A[b](m,k) B[b](n,k) with epilogue `epi`.
 
     A/B majors follow include/jigsaw_sm100.h. fp32 operands run 3xTF32: the hi/lo split is
@@ -123,6 +123,14 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
     if d_planes is not None:
         for i, addr in enumerate(d_planes):
             d.d_planes[i] = addr
+    if rs is not None:
+        # fused reduce-scatter (jg_gemm_desc rs_*): flags / peer flag arrays / partial-plane source
+        d.rs_flags = rs.get("flags")
+        for i, addr in enumerate(rs["flag_peers"]):
+            d.rs_flag_peers[i] = addr
+        d.rs_src, d.rs_src_stride = rs.get("src"), rs.get("src_stride", 0)
+        d.rs_part_type, d.rs_nsrc, d.rs_src_idx = rs["part_type"], rs["nsrc"], rs["src_idx"]
+        d.rs_own, d.rs_need, d.rs_flag_cap = rs.get("own", -1), rs["need"], rs["flag_cap"]
     for fld, addrs in (("d_bcast", d_bcast), ("d2_bcast", d2_bcast)):
         bc = _lib.make_bcast(addrs)
         if bc is not None:
@@ -137,7 +145,7 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
         s.record()
         _lib.gemm_raw(d)
         e.record()
-        ae, oe = a.element_size(), out.element_size()
+        ae, oe = a.element_size(), (out.element_size() if out is not None else 2)
         outs = 1 if reduce_batch else batch
         nbytes = (m * k + n * k) * ae * batch + m * n * oe * outs * (2 if epi & _lib.EPI_ACCUM else 1)
         GEMM_TIMER.append((s, e, 2 * m * n * k * batch, nbytes))

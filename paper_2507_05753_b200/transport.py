@@ -26,6 +26,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from . import kernels as K
 
 
@@ -102,6 +103,16 @@ class NcclTransport:
         return red, 1, 0
 
 
+FLAG_CAP = 1 << 15  # arrival counters per reduce-scatter region (jg_gemm_desc.rs_flag_cap)
+
+
+def fused_rs_enabled() -> bool:
+    """GEMM + reduce-scatter + epilogue as one kernel (JIGSAW_FUSED_RS=0 restores the
+    GEMM -> barrier -> jg_epilogue sequence)."""
+    import os
+    return os.environ.get("JIGSAW_FUSED_RS", "0") == "1"
+
+
 class SymmTransport:
     kind = "symm"
 
@@ -117,8 +128,11 @@ class SymmTransport:
             off += -(-n * torch.empty((), dtype=dtype).element_size() // 256) * 256
         self.scratch_off = off
         self.scratch_bytes = -(-scratch_bytes // 256) * 256
+        self.flag_off = off + 2 * self.scratch_bytes  # per region: FLAG_CAP arrival counters (fused RS)
         self.k = 0
-        self._alloc(off + 2 * self.scratch_bytes)
+        self._alloc(self.flag_off + 2 * FLAG_CAP * 4)
+        self.buf[self.flag_off:].zero_()
+        self.barrier()  # every member's counters are zero before anyone signals
 
     def _alloc(self, total: int) -> None:
         """One symmetric arena per group member; self.base[j] = member j's arena address."""
@@ -195,3 +209,42 @@ class SymmTransport:
             fn(s, local[0], 0, [self.base[j * q + s] + off + self.idx * pbytes for j in range(self.G // q)])
         self.barrier()
         return local, self.G, rows * cols
+
+    def rs_gemm_fused(self, rows: int, cols: int, dtype, fn, q: int = 1, **epi) -> None:
+        """Reduce-scatter fused into the GEMM (jg_gemm_desc rs_*): each launch stores its
+        partial tiles raw into the owners' region slots and counts their arrival on the owners'
+        flags; the launch holding this rank's own plane runs those tiles last, waits per tile for
+        every peer's partial, sums the planes in member order and applies the epilogue `epi`
+        (jg_epilogue's arguments; d = the output) — no barrier, no separate epilogue pass.
+        Region reuse is safe without a barrier: a member writes region k again only two
+        reduce-scatters later, and it cannot finish the one in between before this rank has
+        started it, i.e. finished reading region k (stream order)."""
+        es = torch.empty((), dtype=dtype).element_size()
+        pbytes = rows * cols * es
+        fl = self.flag_off + (self.k % 2) * FLAG_CAP * 4
+        off = self._region()
+        assert self.G * pbytes <= self.scratch_bytes
+        local = self._view(off, (self.G, rows, cols), dtype)
+        d = epi.pop("d")
+        for bad in ("ldd", "ldd2", "ldr", "ldp", "batch", "acc_ld"):
+            assert bad not in epi, f"fused reduce-scatter epilogue: unsupported argument {bad}"
+        part = _lib.dtype_code(local)
+        nb = self.G // q
+        for s in range(q):
+            dpl, fpeers, own = [], [], -1
+            for j in range(nb):
+                o = j * q + s
+                if o == self.idx:
+                    own = j
+                    dpl.append(None)
+                    fpeers.append(None)
+                else:
+                    dpl.append(self.base[o] + off + self.idx * pbytes)
+                    fpeers.append(self.base[o] + fl)
+            rs = dict(flags=self.base[self.idx] + fl if own >= 0 else None, flag_peers=fpeers,
+                      src=self.base[self.idx] + off, src_stride=rows * cols, part_type=part, nsrc=self.G,
+                      src_idx=self.idx, own=own, need=self.G - 1, flag_cap=FLAG_CAP)
+            if own >= 0:
+                fn(s, d, 0, dpl, rs=rs, **epi)
+            else:
+                fn(s, None, 0, dpl, rs=rs)

@@ -87,7 +87,7 @@ def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias
 def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=False, epi=0, alpha=1.0, d2=None,
          bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
          d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None, d_planes=None, d_bcast=None,
-         d2_bcast=None):
+         d2_bcast=None, rs=None):
     lda = lda if lda is not None else (k if am == KM else m)
     ldb = ldb if ldb is not None else (k if bm == KM else n)
     ldd = ldd if ldd is not None else n
@@ -121,6 +121,8 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
             if apb is not None:
                 _view(apb, (m, n), (ldd, 1), ob * d_bs).copy_(w.to(apb.dtype))
         return out
+    if rs is not None:
+        return _gemm_rs(acc, out, m, n, ldd, d_planes, rs, epi, alpha, d2, bias, resid, pre, stats, d_bcast, d2_bcast)
     if d_planes:  # fused reduce-scatter: batch ob's partial goes straight to its owner's plane
         assert epi == 0 and len(d_planes) >= len(acc)
         for ob, v in enumerate(acc):
@@ -131,6 +133,48 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
                         pre, n, p_bs, stats, stats_bs)
     if d_bcast or d2_bcast:
         assert len(acc) == 1
+        _bcast_copy(_view(out, (m, n), (ldd, 1)), d_bcast)
+        if d2 is not None:
+            _bcast_copy(_view(d2, (m, n), (n, 1)), d2_bcast)
+    return out
+
+
+def _flag(addr, slot):
+    return _at(addr + 4 * slot, torch.int32, (1,), (1,))
+
+
+def _gemm_rs(acc, out, m, n, ldd, d_planes, rs, epi, alpha, d2, bias, resid, pre, stats, d_bcast, d2_bcast):
+    """jg_gemm's fused reduce-scatter (include/jigsaw_sm100.h, rs_*) at plane granularity: raw
+    partials to the owners, one arrival flag per sender (slot 1 + sender, written only by that
+    sender), the own plane summed in member order with the partial dtype's rounding, then the
+    epilogue with batch-0 addressing."""
+    import time
+    pdt = torch.bfloat16 if rs["part_type"] == 1 else torch.float32
+    own = rs.get("own", -1) if rs.get("flags") else -1
+    me, G = rs["src_idx"], rs["nsrc"]
+    for ob, v in enumerate(acc):
+        if ob == own:
+            continue
+        _at(d_planes[ob], pdt, (m, n), (ldd, 1)).copy_(v.to(pdt))
+        _flag(rs["flag_peers"][ob], 1 + me).add_(1)
+    if own < 0:
+        return out
+    t0 = time.time()
+    peers = [j for j in range(G) if j != me]
+    while any(int(_flag(rs["flags"], 1 + j).item()) < 1 for j in peers):
+        assert time.time() - t0 < 120, "fused reduce-scatter: a peer never arrived"
+        time.sleep(0.0005)
+    for j in peers:
+        _flag(rs["flags"], 1 + j).sub_(1)
+    es = torch.empty((), dtype=pdt).element_size()
+    tot = torch.zeros(m, n, dtype=torch.float64)
+    for j in range(G):
+        if j == me:
+            tot += acc[own].to(pdt).double()
+        else:
+            tot += _at(rs["src"] + j * rs["src_stride"] * es, pdt, (m, n), (ldd, 1)).double()
+    _apply_epilogue(tot, 0, m, n, epi, alpha, out, ldd, 0, d2, n, 0, bias, 0, resid, n, 0, pre, n, 0, stats, 0)
+    if d_bcast or d2_bcast:
         _bcast_copy(_view(out, (m, n), (ldd, 1)), d_bcast)
         if d2 is not None:
             _bcast_copy(_view(d2, (m, n), (n, 1)), d2_bcast)

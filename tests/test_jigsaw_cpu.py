@@ -39,6 +39,8 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
         import cpu_kernels
         cpu_kernels.install()
         opts = opts or {}
+        if "fused_rs" in opts:
+            os.environ["JIGSAW_FUSED_RS"] = opts["fused_rs"]
         if opts.get("transport") == "shm":
             import shm_transport
             shm_transport.install()
@@ -230,6 +232,14 @@ def test_symmetric_memory_schedule_matches_reference(world):
     """The peer-memory transport's plumbing (slots, rotating partial regions, producer pushes,
     epilogue stores into owners' planes, q-way sub-chunks at 4 x 2) on emulated peer memory."""
     _check(world, opts={"transport": "shm"})
+
+
+@pytest.mark.parametrize("world,fused", [(2, "1"), (4, "1"), (8, "1"), (8, "0")])
+def test_fused_reduce_scatter_schedule_matches_reference(world, fused):
+    """GEMM + reduce-scatter + epilogue as one kernel (jg_gemm rs_*: raw partials to the owners,
+    arrival flags, own plane summed in member order) against the GEMM -> barrier -> epilogue
+    schedule's reference results, including the q = 2 owner sub-chunks of the 4 x 2 grid."""
+    _check(world, opts={"transport": "shm", "fused_rs": fused})
 
 
 def test_symmetric_memory_rollout_8way():

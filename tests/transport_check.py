@@ -39,6 +39,29 @@ for axis in ("row", "col"):
     ssum = sum(sa.reshape(-1)[i * sp:(i + 1) * sp] for i in range(sn)).view(64, 48) if sn > 1 else sa
     na, nn, np_ = nt.rs_gemm(64, 48, torch.float32, fn)
     res.append((axis, "rs", (ssum - na).abs().max().item(), na.abs().max().item()))
+    # GEMM + reduce-scatter + epilogue in one kernel (rs_gemm_fused) == GEMM -> barrier -> jg_epilogue,
+    # bit for bit: multi-tile 2-CTA shapes, fp32 and bf16 partials, plain sum and bias + GELU epilogue
+    rows, cols, kk = 512, 384, 256
+    A2 = torch.randn(G * rows, kk, device=dev).bfloat16()
+    B2 = torch.randn(cols, kk, device=dev).bfloat16()
+    bias = torch.randn(cols, device=dev)
+
+    def fn2(s, D, d_bs, dpl, **kw):
+        K.gemm(D, A2, B2, 0, 0, rows, cols, kk, G, rows * kk, 0, d_bs=d_bs, d_planes=dpl, **kw)
+
+    for pdt in (torch.float32, torch.bfloat16):
+        for epi in (0, _lib.EPI_BIAS_COL | _lib.EPI_GELU_FWD):
+            kw = dict(epi=epi, bias=bias) if epi else {}
+            ref_d, ref_d2 = torch.empty(rows, cols, device=dev), torch.empty(rows, cols, device=dev).bfloat16()
+            sa, sn, sp = st.rs_gemm(rows, cols, pdt, fn2)
+            K.epilogue(sa, rows, cols, acc_bs=sp, nplanes=sn, d=ref_d, d2=ref_d2 if epi else None, **kw)
+            for rep in range(3):  # repeated calls exercise both regions and the flag re-arming
+                got_d, got_d2 = torch.zeros(rows, cols, device=dev), torch.zeros(rows, cols, device=dev).bfloat16()
+                st.rs_gemm_fused(rows, cols, pdt, fn2, d=got_d, d2=got_d2 if epi else None, **kw)
+                err = (got_d - ref_d).abs().max().item()
+                if epi:
+                    err = max(err, (got_d2.float() - ref_d2.float()).abs().max().item())
+                res.append((axis, f"rs_fused_{str(pdt)[6:]}_{epi}_{rep}", err, ref_d.abs().max().item()))
     torch.cuda.synchronize()
 print(rank, res, flush=True)
 bad = [r for r in res if r[2] != 0.0]

@@ -25,7 +25,8 @@ orig = T.gemm_into
 
 def rec(out, a, b, am, bm, m, n, k, batch=1, *args, **kw):
     if T.GEMM_TIMER is not None:
-        shapes.append((m, n, k, batch, bool(kw.get("reduce_batch")), am, bm, kw.get("d_planes") is not None))
+        pe = 2 if kw.get("rs") is not None else int(kw.get("d_planes") is not None)  # 2: fused reduce-scatter
+        shapes.append((m, n, k, batch, bool(kw.get("reduce_batch")), am, bm, pe))
     return orig(out, a, b, am, bm, m, n, k, batch, *args, **kw)
 
 
@@ -37,7 +38,7 @@ T.GEMM_TIMER = []
 step._body()
 torch.cuda.synchronize()
 recs, T.GEMM_TIMER = T.GEMM_TIMER, None
-if comm.rank == 0:
+if comm.rank == int(os.environ.get("PRINT_RANK", "0")):
     tot = sum(a.elapsed_time(b) for a, b, _, _ in recs)
     fl = sum(f for _, _, f, _ in recs)
     print(f"{len(recs)} GEMMs {tot:.3f} ms {fl / tot / 1e9:.0f} TFLOP/s")
