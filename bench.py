@@ -251,13 +251,19 @@ def run_ours(args, rank, world):
     # ---------------- e2e: public API with pinned host buffers ---------------------------
     xh = xd.cpu().pin_memory()
     th = td.cpu().pin_memory()
-    e_steps = max(1, min(args.steps, 5))
+    prefetch = os.environ.get("JIGSAW_E2E_PREFETCH", "1") == "1"
+    step.warm_prefetch()
+    step(xh, th)  # untimed: first public call (lazy stream / buffer set-up)
+    e_steps = max(1, args.steps)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(e_steps):
-        step(xh, th)
+    if prefetch:
+        step.prefetch(xh, th)  # step 0's inputs: copied inside the timed region like every other step's
+    for i in range(e_steps):
+        # each step's H2D copy of the next step's inputs runs behind its compute (prefetch)
+        step(xh, th, prefetch_next=(xh, th) if prefetch and i + 1 < e_steps else None)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -307,7 +313,10 @@ def run_ours(args, rank, world):
             "clocks": clock,
             "e2e": {"value": args.batch / (e2e_ms / 1e3), "unit": "samples/s",
                     "h2d_bytes_per_step": step.h2d_bytes_per_step * world, "d2h_bytes_per_step": step.d2h_bytes_per_step * world,
-                    "ms_per_step": e2e_ms, "api": "TrainStep.__call__(x_host_pinned, target_host_pinned) -> float loss"},
+                    "ms_per_step": e2e_ms,
+                    "api": "TrainStep.__call__(x_host_pinned, target_host_pinned, prefetch_next=(x, target)) -> float loss",
+                    "input_pipelining": ("each step's H2D copy of the next step's inputs overlaps its compute" if prefetch
+                                         else "none: each step copies its own inputs")},
             "gpu_launches": (step.launches_per_step or 0) * args.steps,
             "launches_per_step": step.launches_per_step,
             "fused_adam": step.fused_adam,

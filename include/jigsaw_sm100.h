@@ -54,6 +54,9 @@ extern "C" {
 #define JG_EPI_ADAM 256u    /* result is a complete weight gradient: apply Adam to D = fp32 master
                                in place (m, v, bf16 copy alongside) instead of storing the gradient
                                (fused into the producer; no gradient round trip) */
+#define JG_EPI_LNB 512u     /* the result is the upstream gradient g of a layer norm: accumulate its
+                               backward row moments stats[row] += (sum_col g*gamma, sum_col
+                               g*gamma*xhat), xhat = (x - mean) * rstd  (model.py:242-250) */
 
 /* Extra destinations of an output (the same element offsets relative to each base): used to
  * push a Jigsaw all-gather operand straight from its producer into the peers' NVLink-mapped
@@ -133,6 +136,11 @@ typedef struct jg_gemm_desc {
   uint32_t* rs_flag_peers[8];
   const void* rs_src; int64_t rs_src_stride;
   int32_t rs_part_type, rs_nsrc, rs_src_idx, rs_own, rs_need, rs_flag_cap;
+  /* JG_EPI_LNB operands: the layer norm's input x (fp32, row stride lnb_ldx, batch stride
+   * lnb_x_bstride), gamma [n], (mean, rstd) per row with the stats layout (batch stride
+   * stats_bstride); the moments go to `stats` (zeroed by the caller). */
+  const float* lnb_x; int64_t lnb_ldx, lnb_x_bstride;
+  const float* lnb_gamma; const float* lnb_mr;
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);

@@ -28,6 +28,7 @@ JG_MATH_BF16, JG_MATH_TF32X3 = 0, 1
 EPI_ACCUM, EPI_BIAS_COL, EPI_BIAS_ROW, EPI_RESID = 1, 2, 4, 8
 EPI_GELU_FWD, EPI_GELU_BWD, EPI_COPY_D2, EPI_STATS = 16, 32, 64, 128
 EPI_ADAM = 256
+EPI_LNB = 512
 
 EXPORTED = [
     "jg_gemm", "jg_split_tf32", "jg_split_tf32_2d", "jg_cast_bf16", "jg_gelu_fwd", "jg_gelu_bwd",
@@ -116,6 +117,8 @@ class GemmDesc(ctypes.Structure):
         ("rs_src", ctypes.c_void_p), ("rs_src_stride", ctypes.c_int64),
         ("rs_part_type", ctypes.c_int32), ("rs_nsrc", ctypes.c_int32), ("rs_src_idx", ctypes.c_int32),
         ("rs_own", ctypes.c_int32), ("rs_need", ctypes.c_int32), ("rs_flag_cap", ctypes.c_int32),
+        ("lnb_x", ctypes.c_void_p), ("lnb_ldx", ctypes.c_int64), ("lnb_x_bstride", ctypes.c_int64),
+        ("lnb_gamma", ctypes.c_void_p), ("lnb_mr", ctypes.c_void_p),
     ]
 
 

@@ -84,6 +84,7 @@ struct GemmParams {
   // always follows its peers' partials by at least one wave. nwaves == 0: linear order.
   int num_pos, units, nwaves;
   uint8_t wave_kind[64], wave_idx[64];
+  const float* lnb_x; int64_t lnb_ldx, lnb_x_bs; const float* lnb_gamma; const float* lnb_mr;
   int rs_dbg;              // JG_RS_DBG ablations (timing only, results wrong): 1 no fences, 2 no own wait, 4 no peer loads
 };
 
@@ -457,6 +458,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       float rbias = 0.f;
       if ((tepi & JG_EPI_BIAS_ROW) && row_ok) rbias = p.bias[eb * p.bias_bs + row];
       float s1 = 0.f, s2 = 0.f;
+      float lnb_mean = 0.f, lnb_rstd = 0.f;
+      if ((tepi & JG_EPI_LNB) && row_ok) {
+        lnb_mean = p.lnb_mr[eb * p.stats_bs + static_cast<int64_t>(row) * 2];
+        lnb_rstd = p.lnb_mr[eb * p.stats_bs + static_cast<int64_t>(row) * 2 + 1];
+      }
 
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += CSTEP) {
@@ -561,6 +567,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             const float x = (j < ncol) ? v[j] : 0.f;
             s1 += x;
             s2 += x * x;
+          }
+        }
+        if (epi & JG_EPI_LNB) {
+          // layer-norm backward moments of this gradient: (sum g*gamma, sum g*gamma*xhat)
+          const float* xr = p.lnb_x + eb * p.lnb_x_bs + static_cast<int64_t>(row) * p.lnb_ldx + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float t[8];
+              jgd::load8(xr, g * 8, false, t);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float h = v[g * 8 + j] * __ldg(p.lnb_gamma + col0 + g * 8 + j);
+                s1 += h;
+                s2 += h * ((t[j] - lnb_mean) * lnb_rstd);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) {
+                const float h = v[j] * __ldg(p.lnb_gamma + col0 + j);
+                s1 += h;
+                s2 += h * ((xr[j] - lnb_mean) * lnb_rstd);
+              }
           }
         }
         }  // row_ok: math done
@@ -681,7 +712,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           }
         }
       }
-      if ((tepi & JG_EPI_STATS) && row_ok) {
+      if ((tepi & (JG_EPI_STATS | JG_EPI_LNB)) && row_ok) {
         float* sp = p.stats + eb * p.stats_bs + static_cast<int64_t>(row) * 2;
         atomicAdd(sp, s1);
         atomicAdd(sp + 1, s2);
@@ -875,6 +906,10 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   JG_SHAPE_CHECK(!(epi & JG_EPI_RESID) || (g->resid && out_ok(g->resid, g->ldr, JG_F32)), "jg_gemm: bad resid");
   JG_SHAPE_CHECK(!(epi & JG_EPI_GELU_BWD) || (g->pre && out_ok(g->pre, g->ldp, g->pre_type)), "jg_gemm: bad pre");
   JG_SHAPE_CHECK(!(epi & JG_EPI_STATS) || g->stats, "jg_gemm: STATS without stats buffer");
+  JG_SHAPE_CHECK(!(epi & JG_EPI_LNB) || (g->stats && g->lnb_x && g->lnb_gamma && g->lnb_mr && aligned16(g->lnb_x) &&
+                                         g->lnb_ldx % 4 == 0 && g->lnb_x_bstride % 4 == 0 && !(epi & JG_EPI_STATS) &&
+                                         !(epi & JG_EPI_ADAM)),
+                 "jg_gemm: LNB needs stats, an aligned fp32 x (ld %% 4 == 0), gamma and mean/rstd, and no STATS/ADAM");
   JG_SHAPE_CHECK(!(epi & JG_EPI_ADAM) || (g->d && g->d_type == JG_F32 && g->adam_m && g->adam_v && g->adam_step &&
                                           aligned16(g->adam_m) && aligned16(g->adam_v) &&
                                           !(epi & (JG_EPI_ACCUM | JG_EPI_GELU_FWD | JG_EPI_COPY_D2 | JG_EPI_STATS))),
@@ -939,6 +974,8 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   p.resid = g->resid; p.ldr = g->ldr; p.r_bs = g->r_bstride;
   p.pre = g->pre; p.ldp = g->ldp; p.p_bs = g->p_bstride; p.pre_bf16 = g->pre_type == JG_BF16;
   p.stats = g->stats; p.stats_bs = g->stats_bstride;
+  p.lnb_x = g->lnb_x; p.lnb_ldx = g->lnb_ldx; p.lnb_x_bs = g->lnb_x_bstride;
+  p.lnb_gamma = g->lnb_gamma; p.lnb_mr = g->lnb_mr;
   p.adam_m = g->adam_m; p.adam_v = g->adam_v; p.adam_pbf16 = static_cast<__nv_bfloat16*>(g->adam_pbf16);
   p.adam_step = g->adam_step; p.adam_lr = g->adam_lr; p.adam_b1 = g->adam_beta1; p.adam_b2 = g->adam_beta2;
   p.adam_eps = g->adam_eps;
@@ -1008,6 +1045,7 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   // TMA-store epilogue whenever D is write-only (no read-modify-write of D)
   p.tma_store = !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM)) && (g->d != nullptr || p.remote);
   JG_SHAPE_CHECK(!p.rs_mode || p.tma_store, "jg_gemm: fused reduce-scatter needs the TMA-store epilogue");
+  JG_SHAPE_CHECK(!p.rs_mode || !(epi & JG_EPI_LNB), "jg_gemm: LNB is not supported with a fused reduce-scatter");
   if (p.tma_store) {
     const bool dbf = g->d_type == JG_BF16;
     // per-output-batch maps (d_planes / fused reduce-scatter) address one plane each (batch 0)

@@ -219,22 +219,64 @@ class TrainStep:
         self._updated()
         return self.ws.loss
 
-    def __call__(self, x: torch.Tensor, target: torch.Tensor) -> float:
+    def _streams(self):
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream()
+            self._target_ev = torch.cuda.Event()
+            self._stage = None      # device staging buffers of a prefetched step
+            self._staged = None     # (x, target) host tensors the staging buffers hold
+            self._stage_ev = torch.cuda.Event()
+        return self._copy_stream
+
+    def prefetch(self, x: torch.Tensor, target: torch.Tensor) -> None:
+        """Start the host->device copy of the NEXT step's inputs (pinned host tensors) on the copy
+        stream, into device staging buffers, so it overlaps the step running now; the next call
+        with these same tensors waits for it and moves them into place with one device copy.
+        (Pipelined input feeding, as a training loop with a read-ahead loader does.)"""
+        if self.model.device.type != "cuda":
+            return
+        cs = self._streams()
+        if self._stage is None:  # (allocated once, at the first prefetch; see warm_prefetch)
+            self._stage = (torch.empty_like(self.ws.xin), torch.empty_like(self.target))
+        # after everything queued so far (incl. the device copy consuming the previous staged
+        # inputs), but ahead of the step about to be launched
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            self._stage[0].copy_(x, non_blocking=True)
+            self._stage[1].copy_(target, non_blocking=True)
+            self._stage_ev.record(cs)
+        self._staged = (x, target)
+
+    def warm_prefetch(self) -> None:
+        """Allocate the prefetch staging buffers now (outside any timed region)."""
+        if self.model.device.type == "cuda":
+            self._streams()
+            if self._stage is None:
+                self._stage = (torch.empty_like(self.ws.xin), torch.empty_like(self.target))
+
+    def __call__(self, x: torch.Tensor, target: torch.Tensor, prefetch_next=None) -> float:
         """Public step: copy this step's inputs from (pinned) host memory, run, read the loss.
-        The target is copied on a side stream while the forward runs."""
+        Without a prefetch the target is copied on a side stream while the forward runs (x is
+        needed first). `prefetch_next=(x_next, target_next)` also starts the next step's copies
+        behind this step's compute (see prefetch)."""
         cur = torch.cuda.current_stream() if self.model.device.type == "cuda" else None
         ev = None
         if cur is not None:
-            if getattr(self, "_copy_stream", None) is None:
-                self._copy_stream = torch.cuda.Stream()
-                self._target_ev = torch.cuda.Event()
-            cs = self._copy_stream
-            cs.wait_stream(cur)  # the previous step's loss half has finished reading the target
-            self.ws.xin.copy_(x, non_blocking=True)
-            with torch.cuda.stream(cs):
-                self.target.copy_(target, non_blocking=True)
-                self._target_ev.record(cs)
-            ev = self._target_ev
+            cs = self._streams()
+            if self._staged is not None and self._staged[0] is x and self._staged[1] is target:
+                cur.wait_event(self._stage_ev)
+                self.ws.xin.copy_(self._stage[0], non_blocking=True)
+                self.target.copy_(self._stage[1], non_blocking=True)
+                self._staged = None
+            else:
+                cs.wait_stream(cur)  # the previous step's loss half has finished reading the target
+                self.ws.xin.copy_(x, non_blocking=True)
+                with torch.cuda.stream(cs):
+                    self.target.copy_(target, non_blocking=True)
+                    self._target_ev.record(cs)
+                ev = self._target_ev
+            if prefetch_next is not None:
+                self.prefetch(*prefetch_next)
         else:
             self.ws.xin.copy_(x)
             self.target.copy_(target)

@@ -376,11 +376,13 @@ def backward_grid(m, ws) -> None:
         chan_bwd(m, g, None, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b", gf,
                  dX=hc.own, dyrow=hg.planes, epi=E_GB, pre=ws.c[j], d_bcast=hc.peers)
         g.row.publish(hc)
+        # (dX epilogue: this rank's partial LN2-backward row moments of gv, all-reduced in _ln_bwd)
         chan_bwd(m, g, None, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, b + "ch1.w", b + "ch1.b", hc.own,
-                 dX=ws.gv, dyrow=hc.planes)
+                 dX=ws.gv, dyrow=hc.planes, epi=_lib.EPI_LNB, stats=ws.bst2[j],
+                 lnb=(ws.x2[j], p[b + "ln2.gamma"].data, ws.mr2[j]))
         hx = g.row.dest((M, El), od, slot="gx2")                # g_x2 operand copy -> row group
         m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, hx.own, M, El, E,
-                  row_reduce=ctx.all_reduce_row, bcast=hx.peers)
+                  row_reduce=ctx.all_reduce_row, bcast=hx.peers, moments=False)
         g.row.publish(hx)
         xall = hx.planes.view(m.C, B, Tl, El)
         acol_all = g.col.persistent(f"a_col{j}").view(B, -1, Kl) if m.R > 1 else None

@@ -42,6 +42,7 @@ from .sharding import contiguous_split
 KM, MN = _lib.JG_KMAJOR, _lib.JG_MNMAJOR
 E_ACC, E_BCOL, E_BROW, E_RES = _lib.EPI_ACCUM, _lib.EPI_BIAS_COL, _lib.EPI_BIAS_ROW, _lib.EPI_RESID
 E_GF, E_GB, E_CP, E_ST = _lib.EPI_GELU_FWD, _lib.EPI_GELU_BWD, _lib.EPI_COPY_D2, _lib.EPI_STATS
+E_LNB = _lib.EPI_LNB
 
 DTYPES = {"bf16": torch.bfloat16, "f32": torch.float32}
 
@@ -458,12 +459,15 @@ class WeatherMixerModel:
             self._gemm(out, g_op, ws.ca[j], MN, MN, E, H, M, **kw)
             K.colsum(g, p[b + "ch2.b"].grad, M, E)
             # ch1: gv = gc Wc1 ; dWc1 += gc^T v ; dbc1 += sum gc
-            self._gemm(ws.gv, ws.gc, p[b + "ch1.w"].op, KM, MN, M, E, H)
+            # (epilogue: LN2-backward row moments of gv, so _ln_bwd needs only its apply pass)
+            self._gemm(ws.gv, ws.gc, p[b + "ch1.w"].op, KM, MN, M, E, H, epi=E_LNB, stats=ws.bst2[j],
+                       lnb=(ws.x2[j], p[b + "ln2.gamma"].data, ws.mr2[j]))
             out, kw = self._wgrad(b + "ch1.w")
             self._gemm(out, ws.gc, ws.v[j], MN, MN, H, E, M, **kw)
             K.colsum(ws.gc, p[b + "ch1.b"].grad, M, H)
             # ln2 backward + residual: g_x2 = g + LN2'(gv)
-            self._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], g, ws.gx2, ws.gx2_op, M, E)
+            self._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], g, ws.gx2, ws.gx2_op, M, E,
+                         moments=False)
             # tok2 (weight-first): gh = (g_x2^T W2) * gelu'(h) ; dW2 += sum_b g_x2 a ; db2 += row sums
             self._gemm(ws.gh, ws.gx2_op, p[b + "tok2.w"].op, MN, MN, E, Kd, Tn, B, Tn * E, 0, epi=E_GB, pre=ws.h[j])
             out, kw = self._wgrad(b + "tok2.w")
@@ -472,22 +476,26 @@ class WeatherMixerModel:
                 K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tn, E)
             K.colsum(ws.gh, p[b + "tok1.b"].grad, B * E, Kd)
             # tok1 (TN): gu = W1 gh^T ; dW1 += sum_b u gh
-            self._gemm(ws.gu, p[b + "tok1.w"].op, ws.gh, KM, KM, Tn, E, Kd, B, 0, E * Kd)
+            self._gemm(ws.gu, p[b + "tok1.w"].op, ws.gh, KM, KM, Tn, E, Kd, B, 0, E * Kd, epi=E_LNB,
+                       stats=ws.bst1[j], lnb=(ws.res[j], p[b + "ln1.gamma"].data, ws.mr1[j]))
             out, kw = self._wgrad(b + "tok1.w")
             self._gemm(out, ws.u[j], ws.gh, KM, MN, Tn, Kd, E, B, Tn * E, E * Kd, reduce_batch=True, **kw)
             # ln1 backward + residual: g = g_x2 + LN1'(gu)
-            self._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, g, g_op, M, E)
+            self._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, g, g_op, M, E, moments=False)
         # encoder (NT): dWenc += g^T xp ; db += sum g (the input gradient is not needed, model.py:444-445)
         out, kw = self._wgrad("enc.w")
         self._gemm(out, g_op, ws.xp, MN, MN, E, F, M, **kw)
         K.colsum(g, p["enc.b"].grad, M, E)
 
-    def _ln_bwd(self, x, gin, pre, mr, bst, resid, out, out_op, rows, cols, c_total=None, row_reduce=None, bcast=None):
+    def _ln_bwd(self, x, gin, pre, mr, bst, resid, out, out_op, rows, cols, c_total=None, row_reduce=None, bcast=None,
+                moments=True):
         """Two-phase layer-norm backward + residual add (model.py:242-250): row sums (all-reduced
-        over the row group by `row_reduce` when the normalised axis is split), then apply."""
+        over the row group by `row_reduce` when the normalised axis is split), then apply.
+        moments=False: the GEMM producing `gin` already accumulated them (JG_EPI_LNB)."""
         p = self.params
         c_total = c_total or cols
-        K.ln_bwd_moments(x, gin, p[pre + "gamma"].data, mr, bst, rows, cols)
+        if moments:
+            K.ln_bwd_moments(x, gin, p[pre + "gamma"].data, mr, bst, rows, cols)
         if row_reduce is not None:
             row_reduce(bst)
         if out_op is not None and out_op is not out and out_op.dtype == torch.float32:

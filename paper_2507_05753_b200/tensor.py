@@ -83,7 +83,7 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
               stats_bs: int = 0, d_bs: int | None = None, d2_bs: int | None = None,
               lda: int | None = None, ldb: int | None = None, ldd: int | None = None,
               a_lo: torch.Tensor | None = None, b_lo: torch.Tensor | None = None, adam=None,
-              d_planes=None, d_bcast=None, d2_bcast=None, rs: dict | None = None) -> torch.Tensor:
+              d_planes=None, d_bcast=None, d2_bcast=None, rs: dict | None = None, lnb=None) -> torch.Tensor:
     """Low-level fused GEMM: out[b] (op)= sum_k A[b](m,k) B[b](n,k) with epilogue `epi`.
 
     A/B majors follow include/jigsaw_sm100.h. fp32 operands run 3xTF32: the hi/lo split is
@@ -120,6 +120,12 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
         d.pre, d.ldp, d.p_bstride, d.pre_type = pre.data_ptr(), n, p_bs if p_bs else m * n, _lib.dtype_code(pre)
     if stats is not None:
         d.stats, d.stats_bstride = stats.data_ptr(), stats_bs if stats_bs else 2 * m
+    if lnb is not None:
+        # JG_EPI_LNB: (x [batch][m][ldx] fp32, gamma [n], mean/rstd [batch][m][2]); x batch stride m*ldx
+        lx, lg, lmr = lnb[:3]
+        ldx = lnb[3] if len(lnb) > 3 else n
+        d.lnb_x, d.lnb_ldx, d.lnb_x_bstride = lx.data_ptr(), ldx, m * ldx
+        d.lnb_gamma, d.lnb_mr = lg.data_ptr(), lmr.data_ptr()
     if d_planes is not None:
         for i, addr in enumerate(d_planes):
             d.d_planes[i] = addr

@@ -14,6 +14,7 @@ import torch
 EPI_ACCUM, EPI_BIAS_COL, EPI_BIAS_ROW, EPI_RESID = 1, 2, 4, 8
 EPI_GELU_FWD, EPI_GELU_BWD, EPI_COPY_D2, EPI_STATS = 16, 32, 64, 128
 EPI_ADAM = 256
+EPI_LNB = 512
 KM = 0
 
 
@@ -61,7 +62,7 @@ def _gelu_grad(x):
 
 
 def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias, bias_bs, resid, ldr, r_bs,
-                    pre, ldp, p_bs, stats, stats_bs):
+                    pre, ldp, p_bs, stats, stats_bs, lnb=None):
     v = v * alpha
     if epi & EPI_BIAS_COL:
         v = v + _view(bias, (n,), (1,), ob * bias_bs).double()[None, :]
@@ -82,12 +83,21 @@ def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias
         sv = _view(stats, (m, 2), (2, 1), ob * stats_bs)
         sv[:, 0] += v.sum(1).to(sv.dtype)
         sv[:, 1] += (v * v).sum(1).to(sv.dtype)
+    if epi & EPI_LNB:  # layer-norm backward row moments of the result (jg_gemm JG_EPI_LNB)
+        lx, lg, lmr = lnb[:3]
+        ldx = lnb[3] if len(lnb) > 3 else n
+        x = _view(lx, (m, n), (ldx, 1), ob * m * ldx).double()
+        mr = _view(lmr, (m, 2), (2, 1), ob * stats_bs).double()
+        h = v * lg.double()[None, :n]
+        sv = _view(stats, (m, 2), (2, 1), ob * stats_bs)
+        sv[:, 0] += h.sum(1).to(sv.dtype)
+        sv[:, 1] += (h * (x - mr[:, :1]) * mr[:, 1:]).sum(1).to(sv.dtype)
 
 
 def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=False, epi=0, alpha=1.0, d2=None,
          bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
          d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None, d_planes=None, d_bcast=None,
-         d2_bcast=None, rs=None):
+         d2_bcast=None, rs=None, lnb=None):
     lda = lda if lda is not None else (k if am == KM else m)
     ldb = ldb if ldb is not None else (k if bm == KM else n)
     ldd = ldd if ldd is not None else n
@@ -130,7 +140,7 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
         return out
     for ob, v in enumerate(acc):
         _apply_epilogue(v, ob, m, n, epi, alpha, out, ldd, d_bs, d2, n, d2_bs, bias, bias_bs, resid, n, r_bs,
-                        pre, n, p_bs, stats, stats_bs)
+                        pre, n, p_bs, stats, stats_bs, lnb=lnb)
     if d_bcast or d2_bcast:
         assert len(acc) == 1
         _bcast_copy(_view(out, (m, n), (ldd, 1)), d_bcast)

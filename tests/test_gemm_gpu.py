@@ -131,3 +131,29 @@ def test_reduce_batch(cuda):
                 reduce_batch=True, epi=_lib.EPI_ACCUM)
     ref = torch.einsum("bte,bej->tj", u.double(), gh.double())
     assert rel_err(out.cpu(), ref.cpu()) < 2e-5
+
+
+@pytest.mark.parametrize("batch,m,n,k", [(1, 300, 520, 256), (2, 257, 1032, 192)])
+def test_lnb_epilogue_moments(cuda, batch, m, n, k):
+    """JG_EPI_LNB: the GEMM result g is stored unchanged and its layer-norm-backward row moments
+    (sum g*gamma, sum g*gamma*xhat) land in `stats` (ln_bwd_moments semantics, model.py:242-250),
+    per batch, including ragged row / column tiles and 2-CTA tiles."""
+    from paper_2507_05753_b200 import _lib, tensor as T
+    gen = torch.Generator(device="cpu").manual_seed(11)
+    a = torch.randn(batch, m, k, generator=gen).to(cuda, torch.bfloat16)
+    b = torch.randn(n, k, generator=gen).to(cuda, torch.bfloat16)
+    x = torch.randn(batch, m, n, generator=gen).to(cuda)
+    gamma = torch.randn(n, generator=gen).to(cuda)
+    mr = torch.stack([torch.randn(batch * m, generator=gen), torch.rand(batch * m, generator=gen) + 0.5], 1).to(cuda)
+    out = torch.empty(batch, m, n, device=cuda)
+    stats = torch.zeros(batch * m, 2, device=cuda)
+    T.gemm_into(out, a, b, _lib.JG_KMAJOR, _lib.JG_KMAJOR, m, n, k, batch, m * k, 0, epi=_lib.EPI_LNB,
+                stats=stats, lnb=(x, gamma, mr))
+    torch.cuda.synchronize()
+    ref = (a.double() @ b.double().t())
+    assert rel_err(out.double().cpu().numpy(), ref.cpu().numpy()) < 1e-5
+    g = out.double().reshape(batch * m, n)
+    h = g * gamma.double()[None, :]
+    xhat = (x.double().reshape(batch * m, n) - mr[:, :1].double()) * mr[:, 1:].double()
+    want = torch.stack([h.sum(1), (h * xhat).sum(1)], 1)
+    assert rel_err(stats.double().cpu().numpy(), want.cpu().numpy()) < 1e-5
