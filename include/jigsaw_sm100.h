@@ -168,6 +168,15 @@ int jg_sum_planes(float* y, const void* x, int32_t x_type, int64_t n, int32_t np
  * Used to push Jigsaw activation tiles into peers' symmetric gather buffers. */
 int jg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Device-side barrier of a Jigsaw group over peer memory (graph-capturable; publishes the
+ * producer-push gathers and reduce-scatter partials of the exchanges in parallel.py:118-353).
+ * peer_slots[j] = member j's arrival counters (G uint32, NVLink-mapped), own_slots = this
+ * member's; *epoch (this device) counts the barriers passed. One 32-thread block: epoch += 1,
+ * system-scope release add of 1 into peer_slots[j][idx] for every j != idx, then acquire-spin
+ * until own_slots[j] >= epoch for every j != idx (traps after ~4 s instead of hanging). */
+int jg_group_barrier(uint32_t* const* peer_slots, uint32_t* own_slots, uint32_t* epoch, int32_t G, int32_t idx,
+                     void* stream);   /* G <= 8 */
+
 /* Split fp32 x into tf32-exact hi (low 13 mantissa bits cleared) and lo = x - hi. */
 int jg_split_tf32(const float* x, float* hi, float* lo, int64_t n, void* stream);
 

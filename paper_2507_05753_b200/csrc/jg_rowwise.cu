@@ -3,6 +3,7 @@
 // All are coalesced along the contiguous (last) axis, vectorised to 16-byte accesses where
 // the row length allows, warp-reduced, and grid-sized in multiples of the SM count.
 #include "jg_common.cuh"
+#include <cstring>
 
 namespace {
 
@@ -1214,6 +1215,45 @@ int jg_sum_planes(float* y, const void* x, int32_t x_type, int64_t n, int32_t np
   if (bf) sum_planes_kernel<true><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(y, x, n, nplanes, plane_stride, accumulate != 0, vec);
   else sum_planes_kernel<false><<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(y, x, n, nplanes, plane_stride, accumulate != 0, vec);
   JG_LAUNCH_CHECK("sum_planes");
+  return JG_OK;
+}
+
+struct BarrierArgs { uint32_t* peer[8]; uint32_t* own; uint32_t* epoch; int G, idx; };
+
+__global__ void group_barrier_kernel(const BarrierArgs a) {
+  __shared__ uint32_t e;
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    e = *a.epoch + 1;
+    *a.epoch = e;
+  }
+  __syncthreads();
+  __threadfence_system();  // this GPU's earlier (peer) stores are visible before it signals
+  if (lane < a.G && lane != a.idx) {
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.peer[lane] + a.idx) : "memory");
+    const long long t0 = clock64();
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.own + lane) : "memory");
+      if (static_cast<int32_t>(v - e) >= 0) break;
+      if (clock64() - t0 > (1ll << 33)) __trap();  // a member never arrived: fail loudly
+    }
+  }
+  __syncthreads();
+}
+
+int jg_group_barrier(uint32_t* const* peer_slots, uint32_t* own_slots, uint32_t* epoch, int32_t G, int32_t idx,
+                     void* stream) {
+  JG_SHAPE_CHECK(G >= 1 && G <= 8 && idx >= 0 && idx < G && own_slots && epoch, "jg_group_barrier: bad group");
+  BarrierArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int j = 0; j < G; ++j) a.peer[j] = peer_slots[j];
+  a.own = own_slots;
+  a.epoch = epoch;
+  a.G = G;
+  a.idx = idx;
+  group_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a);
+  JG_LAUNCH_CHECK("group_barrier");
   return JG_OK;
 }
 

@@ -23,6 +23,9 @@ Two implementations of the same two operations used by jigsaw_grid.py:
 """
 from __future__ import annotations
 
+import ctypes
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -107,9 +110,8 @@ FLAG_CAP = 1 << 15  # arrival counters per reduce-scatter region (jg_gemm_desc.r
 
 
 def fused_rs_enabled() -> bool:
-    """GEMM + reduce-scatter + epilogue as one kernel (JIGSAW_FUSED_RS=0 restores the
-    GEMM -> barrier -> jg_epilogue sequence)."""
-    import os
+    """GEMM + reduce-scatter + epilogue as one kernel (JIGSAW_FUSED_RS=1; the default is the
+    GEMM -> barrier -> jg_epilogue sequence, measured faster)."""
     return os.environ.get("JIGSAW_FUSED_RS", "0") == "1"
 
 
@@ -129,10 +131,17 @@ class SymmTransport:
         self.scratch_off = off
         self.scratch_bytes = -(-scratch_bytes // 256) * 256
         self.flag_off = off + 2 * self.scratch_bytes  # per region: FLAG_CAP arrival counters (fused RS)
+        self.bar_off = self.flag_off + 2 * FLAG_CAP * 4  # G arrival counters of jg_group_barrier
         self.k = 0
-        self._alloc(self.flag_off + 2 * FLAG_CAP * 4)
+        self._alloc(self.bar_off + 256)
         self.buf[self.flag_off:].zero_()
+        # JIGSAW_BARRIER=jg: jg_group_barrier (one 32-thread kernel: release-add into each peer's
+        # counter, acquire-spin on its own); measured no faster than the default, torch's barrier
+        self._jg_bar = False
         self.barrier()  # every member's counters are zero before anyone signals
+        self._jg_bar = os.environ.get("JIGSAW_BARRIER", "torch") == "jg"
+        self._bar_peers = (ctypes.c_void_p * 8)(*[b + self.bar_off for b in self.base])
+        self._bar_epoch = torch.zeros(1, dtype=torch.int32, device=device)
 
     def _alloc(self, total: int) -> None:
         """One symmetric arena per group member; self.base[j] = member j's arena address."""
@@ -166,7 +175,11 @@ class SymmTransport:
         return r
 
     def barrier(self) -> None:
-        self.hdl.barrier(channel=0)
+        if self._jg_bar:
+            _lib.call("jg_group_barrier", self._bar_peers, self.base[self.idx] + self.bar_off,
+                      self._bar_epoch.data_ptr(), self.G, self.idx)
+        else:
+            self.hdl.barrier(channel=0)
 
     def _slot_off(self, slot: str, sub: int, nbytes: int) -> int:
         off, shape, dtype = self.offsets[slot]
