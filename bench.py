@@ -261,13 +261,22 @@ def run_ours(args, rank, world):
     e0.record(stream)
     if prefetch:
         step.prefetch(xh, th)  # step 0's inputs: copied inside the timed region like every other step's
+    marks = []
     for i in range(e_steps):
         # each step's H2D copy of the next step's inputs runs behind its compute (prefetch)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
         step(xh, th, prefetch_next=(xh, th) if prefetch and i + 1 < e_steps else None)
+        eb.record(stream)
+        marks.append((ea, eb))
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e_steps
+    # device time inside the calls vs the GPU idling between them (host turnaround: loss read,
+    # Python, graph launches) — diagnostics for the e2e / value gap
+    call_ms = sum(a.elapsed_time(b) for a, b in marks) / e_steps
+    e2e_call_ms = max_over_ranks(call_ms)
 
     # ---------------- roofline of the dominant kernel (jg_gemm) --------------------------
     # one eager step with per-launch CUDA events on the launching stream
@@ -313,7 +322,7 @@ def run_ours(args, rank, world):
             "clocks": clock,
             "e2e": {"value": args.batch / (e2e_ms / 1e3), "unit": "samples/s",
                     "h2d_bytes_per_step": step.h2d_bytes_per_step * world, "d2h_bytes_per_step": step.d2h_bytes_per_step * world,
-                    "ms_per_step": e2e_ms,
+                    "ms_per_step": e2e_ms, "device_ms_per_call": e2e_call_ms,
                     "api": "TrainStep.__call__(x_host_pinned, target_host_pinned, prefetch_next=(x, target)) -> float loss",
                     "input_pipelining": ("each step's H2D copy of the next step's inputs overlaps its compute" if prefetch
                                          else "none: each step copies its own inputs")},

@@ -70,7 +70,7 @@ class GridWorkspace:
         self.panel_names = [n for n in m.params if _base(n) in CHANNEL_LAYERS] if R > 1 else []
         nmax = max(E, H, F)
         row_persist = [(f"u_row{j}", (C, B, Tl, El), od) for j in range(nj)]  # plane-major: LN writes its plane
-        row_persist += [("g", (C, M, El), od), ("gc", (C, M, Hl), od), ("gx2", (C, M, El), od),
+        row_persist += [("g", (C, M, El), od), ("gc", (C, M, Hl), od), ("gx2", (C, M, El), od), ("gd", (C, M, Fl), od),
                         ("tmp", (C, M, nmax // C), od)]
         col_persist = [("tmp", (R, max(E * Kl, max(E * Fl, H * El, E * Hl, F * El) // R)), od)]
         if R > 1:
@@ -365,7 +365,9 @@ def backward_grid(m, ws) -> None:
     gf = ws.g
     # decoder: g = gd Wdec, its operand copy pushed to the row group for ch2's backward
     hg = g.row.dest((M, El), od, slot="g")
-    chan_bwd(m, g, ws.gd, ws.y_op, _panel(m, g, "dec.w"), M, El, F, "dec.w", "dec.b", ws.gd, dX=gf,
+    hd = getattr(ws, "gd_row", None)  # the loss kernel already pushed gd to the row group
+    gd, gdrow, gsrc = (None, hd.planes, hd.own) if hd is not None else (ws.gd, None, ws.gd)
+    chan_bwd(m, g, gd, ws.y_op, _panel(m, g, "dec.w"), M, El, F, "dec.w", "dec.b", gsrc, dX=gf, dyrow=gdrow,
              epi=E_CP, d2=hg.own, d2_bcast=hg.peers)
     g.row.publish(hg)
     nj = ws.r * cfg.n_blocks

@@ -396,9 +396,20 @@ class WeatherMixerModel:
         lat, lon = self.local_grid
         bw = self.params["blend.w"]
         want_grad = g_ext is not None or target is not None
+        gd, hd = (ws.gd if want_grad else None), None
+        if want_grad and self.ctx.n > 1 and self.C > 1:
+            # Jigsaw: the decoder-output gradient goes straight into the row group's gather slot
+            # (own plane + peer planes, stored by this kernel) for the decoder's backward GEMMs
+            from .jigsaw_grid import _gw
+            g = _gw(self, ws)
+            hd = g.row.dest((ws.B * ws.Tl, ws.Fl), self.op_dtype, slot="gd")
+            gd = hd.own.view(ws.gd.shape)
         K.blend_loss(ws.dec, ws.xin, target, bw.data, ws.lat_w, ws.var_w, g_ext, out, loss,
-                     bw.grad if want_grad else None, ws.gd if want_grad else None, ws.B, lat, lon, self.local_vars,
-                     cfg.patch[0], cfg.patch[1], ws.inv_count, loss_scale)
+                     bw.grad if want_grad else None, gd, ws.B, lat, lon, self.local_vars,
+                     cfg.patch[0], cfg.patch[1], ws.inv_count, loss_scale, bcast=hd.peers if hd is not None else None)
+        if hd is not None:
+            g.row.publish(hd)
+        ws.gd_row = hd
 
     # -- weight-gradient sink ---------------------------------------------------------------
     def _wgrad(self, name):
