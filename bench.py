@@ -37,7 +37,20 @@ CONFIGS = {
            "WeatherMixer 1.40625 deg (128x256, 69->72 ch, 12 blocks)"),
     "C4": (dict(n_vars=70, grid=(728, 1440), patch=(8, 8), d_emb=4320, d_tok=8640, d_ch=4320, n_blocks=3), 721, 69,
            "WeatherMixer 0.25 deg ERA5-shaped (721->728 x 1440, 69->70 ch, 3 blocks, 1.0B params)"),
+    # weak scaling (BASELINE configs[4]): wide MLPs, n_blocks = n / 2 so the per-GPU
+    # parameters (~0.4B) and FLOPs stay roughly constant: 0.87B / 1.65B / 3.21B params at 2 / 4 / 8
+    "C5": (dict(n_vars=70, grid=(728, 1440), patch=(8, 8), d_emb=10352, d_tok=17280, d_ch=10352, n_blocks=1), 721, 69,
+           "multi-billion-parameter WeatherMixer (0.25 deg, d_emb 10352, d_tok 17280, n/2 blocks; weak scaling)"),
 }
+WEAK = {"C5"}
+
+
+def config_for(name: str, world: int):
+    """(ModelConfig kwargs, real rows, real vars, description) at this world size."""
+    cfg_kw, lat_real, vars_real, desc = CONFIGS[name]
+    if name == "C5":
+        cfg_kw = dict(cfg_kw, n_blocks=max(1, world // 2))
+    return cfg_kw, lat_real, vars_real, desc
 
 
 def parse():
@@ -145,7 +158,7 @@ def cpu_reference_sample(cfg_kw, batch):
 
 
 def run_reference(args, rank, world):
-    cfg_kw, lat_real, vars_real, desc = CONFIGS[args.config]
+    cfg_kw, lat_real, vars_real, desc = config_for(args.config, world)
     if rank != 0:
         return
     from oracle import model as om
@@ -171,7 +184,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {desc}", "batch": args.batch, "parallelism": "cpu (reference algorithm)"},
-        "tflops": om.train_flops(oc, args.batch) * value / 1e12,
+        "tflops": om.train_flops(oc, args.batch) / t_step / 1e12,
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -204,7 +217,7 @@ def run_ours(args, rank, world):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     comm = Communicator.from_env()
-    cfg_kw, lat_real, vars_real, desc = CONFIGS[args.config]
+    cfg_kw, lat_real, vars_real, desc = config_for(args.config, world)
     cfg = ModelConfig(**cfg_kw)
     ctx = MpContext(comm, list(range(world)))
     big = cfg.train_flops() > 1e12
@@ -297,14 +310,15 @@ def run_ours(args, rank, world):
     burst, sustained, hbm, peak_kind = peaks()
     flops_step = cfg.train_flops(args.batch)
     samples_s = args.batch / (ms / 1e3)
-    tflops = flops_step * samples_s / 1e12
+    tflops = flops_step / (ms / 1e3) / 1e12  # FLOPs of one step (all B samples) per second
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 / world * world  # per-rank GEMM rate
     line = None
     if rank == 0:
         line = {
             "metric": "WeatherMixer train samples/s", "value": samples_s, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+            "higher_is_better": True, "scaling": "weak" if args.config in WEAK else "strong", "vs_baseline": None,
+            "dtype": args.dtype,
             "data": "synthetic (x, target ~ N(0,1), ERA5-shaped, random-init weights)",
             "config": {"workload": f"{args.config}: {desc}", "batch": args.batch, "grid_padded": list(cfg.grid),
                        "tokens": cfg.tokens, "params": model.param_elements() * world,

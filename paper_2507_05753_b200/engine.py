@@ -24,6 +24,16 @@ from .model import WeatherMixerModel
 from .train import AdamConfig
 
 
+def split_push(lo: int, hi: int, segs, max_segs: int):
+    """Split the Adam range [lo, hi) at panel-segment starts so that each jg_adam_push call
+    carries at most `max_segs` segments (e.g. 12 blocks = 26 channel-mixing panels at R > 1).
+    segs: [(start - lo, numel, addrs)]; yields (a0, a1, segments re-based to a0)."""
+    segs = sorted(segs, key=lambda t: t[0])
+    cuts = [lo] + [lo + segs[j][0] for j in range(max_segs, len(segs), max_segs)]
+    for a0, a1 in zip(cuts, cuts[1:] + [hi]):
+        yield a0, a1, [(st - (a0 - lo), n, addrs) for st, n, addrs in segs if a0 <= lo + st < a1]
+
+
 class TrainStep:
     def __init__(self, model: WeatherMixerModel, batch: int = 1, r: int = 1, adam: AdamConfig | None = None,
                  graph: bool = True, loss_scale: float = 1.0, fused_adam: bool = False,
@@ -148,11 +158,12 @@ class TrainStep:
                 lo, hi = f.vec_range(cls)
             if hi <= lo:
                 continue
-            K.adam(f.master[lo:], f.grad[lo:], f.m[lo:], f.v[lo:], None if op_copy is None else op_copy[lo:],
-                   hi - lo, a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count,
-                   grad_scale=self.grad_scale if self.clip is not None else None,
-                   lr_dev=self.lr_dev[i:i + 1] if self.scheduled else None,
-                   push=panel_push_segments(self.model, self.ws.grid, lo, hi) if push else None)
+            segs = panel_push_segments(self.model, self.ws.grid, lo, hi) if push else []
+            for a0, a1, sub in split_push(lo, hi, segs, _lib.JG_MAX_PUSH_SEGS):
+                K.adam(f.master[a0:], f.grad[a0:], f.m[a0:], f.v[a0:], None if op_copy is None else op_copy[a0:],
+                       a1 - a0, a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count,
+                       grad_scale=self.grad_scale if self.clip is not None else None,
+                       lr_dev=self.lr_dev[i:i + 1] if self.scheduled else None, push=sub or None)
 
     def _refresh_panels(self) -> None:
         """Before a step whose forward relies on pushed panels: if the weights changed since this

@@ -233,3 +233,20 @@ def test_tile_loader_reads_rank_tiles_with_padding(tmp_path):
     assert set(shares[0]) | set(shares[1]) <= set(base)
     with pytest.raises(ConfigError):
         TileLoader(src[:, :, :32], cfg, SimpleNamespace(R=1, C=1, r=0, c=0), pin=False)
+
+
+def test_adam_push_split_respects_segment_limit():
+    """26 panel segments (12 blocks at R > 1) -> Adam calls of <= 16 segments each, covering
+    the class range exactly once, segments re-based to their call and never split."""
+    from paper_2507_05753_b200.engine import split_push
+    lo, hi = 1000, 1000 + 26 * 100 + 37
+    segs = [(i * 100 + 5, 90, [i]) for i in reversed(range(26))]
+    calls = list(split_push(lo, hi, segs, 16))
+    assert calls[0][0] == lo and calls[-1][1] == hi
+    assert all(a1 == b0 for (_, a1, _), (b0, _, _) in zip(calls, calls[1:]))
+    assert all(len(sub) <= 16 for _, _, sub in calls)
+    got = sorted((a0 + st, n, tuple(ad)) for a0, a1, sub in calls for st, n, ad in sub)
+    assert got == sorted((lo + st, n, tuple(ad)) for st, n, ad in segs)
+    for a0, a1, sub in calls:
+        assert all(0 <= st and a0 + st + n <= a1 for st, n, _ in sub)
+    assert list(split_push(lo, hi, [], 16)) == [(lo, hi, [])]

@@ -51,3 +51,20 @@ def test_captured_train_step_multi_gpu(n):
            "--master-addr=127.0.0.1", "--master-port=29565", os.path.join(HERE, "train_mp_check.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert "TRAINMP_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_bench_many_blocks_multi_gpu(n):
+    """The captured Jigsaw step at C3 (12 blocks: 26 channel-mixing weight panels pushed by Adam,
+    more than one jg_adam_push call per lr class) runs through bench.py and reports a finite loss."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29567", os.path.join(root, "bench.py"), "--gpus", str(n),
+           "--config", "C3", "--batch", "2", "--steps", "2", "--warmup", "1"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert p.returncode == 0 and lines, p.stdout[-2000:] + p.stderr[-3000:]
+    d = json.loads(lines[-1])
+    assert d["n_gpus"] == n and d["value"] > 0 and abs(d["config"]["loss"]) < 1e3
