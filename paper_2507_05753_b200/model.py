@@ -28,6 +28,8 @@ reduce-scatter schedule of parallel.py through NCCL on the compute stream.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -566,11 +568,14 @@ class _Workspace:
         self.bst2 = [self.bstats[2 * j + 1] for j in range(nj)]
         self.res = [torch.empty((B, Tl, El), **f32) for _ in range(nj + 1)]
         self.u = [torch.empty((B, Tl, El), **opk) for _ in range(nj)]
-        self.h = [torch.empty((B, Er, Kl), **f32) for _ in range(nj)]
+        # GELU pre-activations (kept only for GELU' in the backward): operand dtype, i.e. bf16 in
+        # bf16 mode — half the epilogue stores and backward reads (JIGSAW_PRE_FP32=1 keeps fp32)
+        prek = f32 if os.environ.get("JIGSAW_PRE_FP32", "0") == "1" else opk
+        self.h = [torch.empty((B, Er, Kl), **prek) for _ in range(nj)]
         self.a = [torch.empty((B, Er, Kl), **opk) for _ in range(nj)]
         self.x2 = [torch.empty((B, Tl, El), **f32) for _ in range(nj)]
         self.v = [torch.empty((B, Tl, El), **opk) for _ in range(nj)]
-        self.c = [torch.empty((B, Tl, Hl), **f32) for _ in range(nj)]
+        self.c = [torch.empty((B, Tl, Hl), **prek) for _ in range(nj)]
         self.ca = [torch.empty((B, Tl, Hl), **opk) for _ in range(nj)]
         self.y_op = self.res[nj] if od == torch.float32 else torch.empty((B, Tl, El), **opk)
         self.dec = torch.empty((B, Tl, Fl), **f32)
