@@ -211,10 +211,13 @@ int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const 
                       float* bstats, int64_t rows, int64_t cols, void* stream);
 /* backward phase 1: dx = inv_std*(h - sum_h/c_total - xhat*sum_hx/c_total);
  * out = (resid ? resid : 0) + dx  (fp32), out_bf16 optional copy;
- * dgamma[c] += sum_r g*xhat ; dbeta[c] += sum_r g ; rowsum_out[r] += sum_c out (optional). */
+ * dgamma[c] += sum_r g*xhat ; dbeta[c] += sum_r g ;
+ * optional, in the same pass over out (the bias gradients of the layers it feeds,
+ * parallel.py:536, 548): rowsum_out[r % rowsum_period] += sum_c out  (tok2's row bias; the
+ * period folds a batch of samples onto one bias), colsum_out[c] += sum_r out (a column bias). */
 int jg_ln_bwd_apply(const float* x, const float* g, const float* gamma, const float* mean_rstd,
                     const float* bstats, const float* resid, float* out, void* out_bf16,
-                    float* dgamma, float* dbeta, float* rowsum_out,
+                    float* dgamma, float* dbeta, float* rowsum_out, int64_t rowsum_period, float* colsum_out,
                     int64_t rows, int64_t cols, int64_t c_total, const jg_bcast* op_bcast, void* stream);
 
 /* Column sums (bias gradients, parallel.py:548,559-561): out[c] += sum_r x[r*ld + c];

@@ -148,7 +148,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_ln_moments": [vp, vp, i64, i64, i64, vp],
         "jg_ln_apply": [vp, vp, vp, vp, vp, i32, vp, i64, i64, i64, f32, vp, vp],
         "jg_ln_bwd_moments": [vp, vp, vp, vp, vp, i64, i64, vp],
-        "jg_ln_bwd_apply": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, vp, vp],
+        "jg_ln_bwd_apply": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, i64, vp, vp],
         "jg_colsum": [vp, i32, vp, i64, i64, i64, vp],
         "jg_rowsum": [vp, i32, vp, i64, i64, i64, vp],
         "jg_patchify": [vp, vp, i32, i64, i64, i64, i64, i64, i64, vp],

@@ -251,15 +251,19 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
                                     const float* __restrict__ gamma, const float* __restrict__ mean_rstd,
                                     const float* __restrict__ bstats, const float* __restrict__ resid,
                                     float* __restrict__ out, __nv_bfloat16* __restrict__ out_bf16,
-                                    float* __restrict__ dgamma, float* __restrict__ dbeta, int64_t rows, int64_t cols,
+                                    float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                    float* __restrict__ rowsum_out, int64_t rowsum_period,
+                                    float* __restrict__ colsum_out, int64_t rows, int64_t cols,
                                     float inv_ctotal, const Bcast bc) {
   const int64_t c0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
   const int64_t r0 = blockIdx.y * (int64_t)LNB_ROWS;
-  if (c0 >= cols) return;
+  const int lane = threadIdx.x & 31;
+  // threads past the last column stay (nc = 0) so whole warps reduce the row sums
+  const int nc = c0 >= cols ? 0 : (cols - c0 >= 4 ? 4 : static_cast<int>(cols - c0));
+  if (nc == 0 && !rowsum_out) return;
   const int64_t r1 = r0 + LNB_ROWS < rows ? r0 + LNB_ROWS : rows;
-  const int nc = cols - c0 >= 4 ? 4 : static_cast<int>(cols - c0);
   const bool v4 = nc == 4 && (cols % 4 == 0);
-  float gm[4], dg[4] = {0, 0, 0, 0}, db[4] = {0, 0, 0, 0};
+  float gm[4], dg[4] = {0, 0, 0, 0}, db[4] = {0, 0, 0, 0}, cs[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < 4; ++j) gm[j] = j < nc ? gamma[c0 + j] : 0.f;
   for (int64_t rb = r0; rb < r1; rb += LNB_U) {
@@ -306,8 +310,17 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
         if (j < nc) {
           dg[j] += gv[u][j] * xh;
           db[j] += gv[u][j];
+          cs[j] += ov[j];
         }
       }
+      if (rowsum_out) {
+        float rs = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rs += j < nc ? ov[j] : 0.f;
+        rs = warp_sum(rs);
+        if (lane == 0) atomicAdd(rowsum_out + r % rowsum_period, rs);
+      }
+      if (nc == 0) continue;
       if (v4) {
         *reinterpret_cast<float4*>(out + o) = make_float4(ov[0], ov[1], ov[2], ov[3]);
         if (out_bf16) {
@@ -336,6 +349,7 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
     if (j < nc) {
       if (dgamma) atomicAdd(dgamma + c0 + j, dg[j]);
       if (dbeta) atomicAdd(dbeta + c0 + j, db[j]);
+      if (colsum_out) atomicAdd(colsum_out + c0 + j, cs[j]);
     }
   if (bc.n) __threadfence_system();
 }
@@ -992,19 +1006,18 @@ int jg_ln_bwd_moments(const float* x, const float* g, const float* gamma, const 
 
 int jg_ln_bwd_apply(const float* x, const float* g, const float* gamma, const float* mean_rstd, const float* bstats,
                     const float* resid, float* out, void* out_bf16, float* dgamma, float* dbeta, float* rowsum_out,
-                    int64_t rows, int64_t cols, int64_t c_total, const jg_bcast* op_bcast, void* stream) {
+                    int64_t rowsum_period, float* colsum_out, int64_t rows, int64_t cols, int64_t c_total,
+                    const jg_bcast* op_bcast, void* stream) {
   JG_SHAPE_CHECK(rows >= 0 && cols > 0 && c_total >= cols, "jg_ln_bwd_apply: bad shape");
   JG_SHAPE_CHECK(al16(x) && al16(g) && al16(out) && (!resid || al16(resid)), "jg_ln_bwd_apply: pointers must be 16B aligned");
   if (rows == 0) return JG_OK;
   dim3 grid((unsigned)((cols + 1023) / 1024), (unsigned)((rows + LNB_ROWS - 1) / LNB_ROWS));
+  JG_SHAPE_CHECK(!rowsum_out || rowsum_period > 0, "jg_ln_bwd_apply: rowsum_period must be > 0");
   ln_bwd_apply_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, g, gamma, mean_rstd, bstats, resid, out,
-                                                               (__nv_bfloat16*)out_bf16, dgamma, dbeta, rows, cols,
+                                                               (__nv_bfloat16*)out_bf16, dgamma, dbeta, rowsum_out,
+                                                               rowsum_out ? rowsum_period : 1, colsum_out, rows, cols,
                                                                1.0f / (float)c_total, to_bcast(op_bcast));
   JG_LAUNCH_CHECK("ln_bwd_apply");
-  if (rowsum_out) {
-    rowsum_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(out, false, rowsum_out, rows, cols, cols);
-    JG_LAUNCH_CHECK("rowsum");
-  }
   return JG_OK;
 }
 

@@ -203,7 +203,8 @@ def chan_bwd(m, g, dY, X, panel, M, kin_l, nout, wname, bname, bias_src, dX=None
         else:
             acc, npl, ps = g.col.rs_gemm(nr, kin_l, g.pdt, fn, q=q)
             _wgrad_planes(m, g, wname, acc, npl, ps, nr * kin_l)
-    K.colsum(bias_src, m.params[bname].grad, M, nl)
+    if bias_src is not None:  # (None: the layer-norm backward pass that produced dY summed it)
+        K.colsum(bias_src, m.params[bname].grad, M, nl)
 
 
 # --------------------------------------------------------------------------- token layers
@@ -279,7 +280,6 @@ def tok2_bwd(m, g, ws, j, bi, b, grow, acol):
             K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, **epi)
         g.col.publish(hg)
         gh_local, ghcol = hg.own, hg.planes.view(-1, Kl)
-    K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tl, El)
     out, kw = m._wgrad(b + "tok2.w") if bi == 0 or B == 1 else (p[b + "tok2.w"].grad, {"epi": E_ACC})
     if bi == 0 and B > 1 and kw.get("epi") == _lib.EPI_ADAM:
         out, kw = p[b + "tok2.w"].grad, {"epi": E_ACC}
@@ -375,7 +375,8 @@ def backward_grid(m, ws) -> None:
         b = f"block{j % cfg.n_blocks}."
         # ch2: gc = (g Wc2) * gelu'(c), pushed to the row group for ch1's backward
         hc = g.row.dest((M, Hl), od, slot="gc")
-        chan_bwd(m, g, None, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b", gf,
+        chan_bwd(m, g, None, ws.ca[j], _panel(m, g, b + "ch2.w"), M, Hl, E, b + "ch2.w", b + "ch2.b",
+                 gf if j == nj - 1 else None,
                  dX=hc.own, dyrow=hg.planes, epi=E_GB, pre=ws.c[j], d_bcast=hc.peers)
         g.row.publish(hc)
         # (dX epilogue: this rank's partial LN2-backward row moments of gv, all-reduced in _ln_bwd)
@@ -383,8 +384,10 @@ def backward_grid(m, ws) -> None:
                  dX=ws.gv, dyrow=hc.planes, epi=_lib.EPI_LNB, stats=ws.bst2[j],
                  lnb=(ws.x2[j], p[b + "ln2.gamma"].data, ws.mr2[j]))
         hx = g.row.dest((M, El), od, slot="gx2")                # g_x2 operand copy -> row group
+        # (same pass: tok2's row-bias gradient partial = row sums of this rank's g_x2 columns)
         m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, hx.own, M, El, E,
-                  row_reduce=ctx.all_reduce_row, bcast=hx.peers, moments=False)
+                  row_reduce=ctx.all_reduce_row, bcast=hx.peers, moments=False,
+                  sums=dict(rowsum=p[b + "tok2.b"].grad, rowsum_period=Tl))
         g.row.publish(hx)
         xall = hx.planes.view(m.C, B, Tl, El)
         acol_all = g.col.persistent(f"a_col{j}").view(B, -1, Kl) if m.R > 1 else None
@@ -397,10 +400,12 @@ def backward_grid(m, ws) -> None:
         for bi in range(B):
             tok1_bwd(m, g, ws, j, bi, b, ghcols[bi])
         hg = g.row.dest((M, El), od, slot="g")                  # g operand copy -> row group
+        # (same pass: column sums of g = the bias gradient of the previous block's ch2 / the encoder)
+        nxt = f"block{(j - 1) % cfg.n_blocks}.ch2.b" if j > 0 else "enc.b"
         m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, hg.own, M, El, E,
-                  row_reduce=ctx.all_reduce_row, bcast=hg.peers)
+                  row_reduce=ctx.all_reduce_row, bcast=hg.peers, sums=dict(colsum=p[nxt].grad))
         g.row.publish(hg)
-    chan_bwd(m, g, None, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, "enc.w", "enc.b", gf, dyrow=hg.planes)
+    chan_bwd(m, g, None, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, "enc.w", "enc.b", None, dyrow=hg.planes)
 
 
 def grad_sync(m) -> None:

@@ -90,10 +90,11 @@ def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
 
 
 def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total,
-                 bcast=None):
+                 bcast=None, rowsum=None, rowsum_period=0, colsum=None):
+    """rowsum[r % rowsum_period] += sum_c out, colsum[c] += sum_r out, in the same pass (bias grads)."""
     _lib.call("jg_ln_bwd_apply", x.data_ptr(), g.data_ptr(), gamma.data_ptr(), mean_rstd.data_ptr(),
               bstats.data_ptr(), ptr(resid), out.data_ptr(), None if out_op is None or out_op is out else out_op.data_ptr(),
-              ptr(dgamma), ptr(dbeta), None, rows, cols, c_total, _bref(bcast))
+              ptr(dgamma), ptr(dbeta), ptr(rowsum), int(rowsum_period), ptr(colsum), rows, cols, c_total, _bref(bcast))
 
 
 def colsum(x, out, rows, cols, ld=None):

@@ -470,7 +470,8 @@ class WeatherMixerModel:
             self._gemm(ws.gc, g_op, p[b + "ch2.w"].op, KM, MN, M, H, E, epi=E_GB, pre=ws.c[j])
             out, kw = self._wgrad(b + "ch2.w")
             self._gemm(out, g_op, ws.ca[j], MN, MN, E, H, M, **kw)
-            K.colsum(g, p[b + "ch2.b"].grad, M, E)
+            if j == nj - 1:  # (later blocks get this column sum from the LN1-backward pass below)
+                K.colsum(g, p[b + "ch2.b"].grad, M, E)
             # ch1: gv = gc Wc1 ; dWc1 += gc^T v ; dbc1 += sum gc
             # (epilogue: LN2-backward row moments of gv, so _ln_bwd needs only its apply pass)
             self._gemm(ws.gv, ws.gc, p[b + "ch1.w"].op, KM, MN, M, E, H, epi=E_LNB, stats=ws.bst2[j],
@@ -479,14 +480,13 @@ class WeatherMixerModel:
             self._gemm(out, ws.gc, ws.v[j], MN, MN, H, E, M, **kw)
             K.colsum(ws.gc, p[b + "ch1.b"].grad, M, H)
             # ln2 backward + residual: g_x2 = g + LN2'(gv)
+            # (same pass: tok2's row-bias gradient = row sums of g_x2, folded over the B samples)
             self._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], g, ws.gx2, ws.gx2_op, M, E,
-                         moments=False)
+                         moments=False, sums=dict(rowsum=p[b + "tok2.b"].grad, rowsum_period=Tn))
             # tok2 (weight-first): gh = (g_x2^T W2) * gelu'(h) ; dW2 += sum_b g_x2 a ; db2 += row sums
             self._gemm(ws.gh, ws.gx2_op, p[b + "tok2.w"].op, MN, MN, E, Kd, Tn, B, Tn * E, 0, epi=E_GB, pre=ws.h[j])
             out, kw = self._wgrad(b + "tok2.w")
             self._gemm(out, ws.gx2_op, ws.a[j], KM, MN, Tn, Kd, E, B, Tn * E, E * Kd, reduce_batch=True, **kw)
-            for bi in range(B):
-                K.rowsum(ws.gx2[bi], p[b + "tok2.b"].grad, Tn, E)
             K.colsum(ws.gh, p[b + "tok1.b"].grad, B * E, Kd)
             # tok1 (TN): gu = W1 gh^T ; dW1 += sum_b u gh
             self._gemm(ws.gu, p[b + "tok1.w"].op, ws.gh, KM, KM, Tn, E, Kd, B, 0, E * Kd, epi=E_LNB,
@@ -494,14 +494,17 @@ class WeatherMixerModel:
             out, kw = self._wgrad(b + "tok1.w")
             self._gemm(out, ws.u[j], ws.gh, KM, MN, Tn, Kd, E, B, Tn * E, E * Kd, reduce_batch=True, **kw)
             # ln1 backward + residual: g = g_x2 + LN1'(gu)
-            self._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, g, g_op, M, E, moments=False)
+            # (same pass: the column sums of g = the bias gradient of the next layer down — the
+            # previous block's ch2, or the encoder)
+            nxt = f"block{(j - 1) % cfg.n_blocks}.ch2.b" if j > 0 else "enc.b"
+            self._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, g, g_op, M, E, moments=False,
+                         sums=dict(colsum=p[nxt].grad))
         # encoder (NT): dWenc += g^T xp ; db += sum g (the input gradient is not needed, model.py:444-445)
         out, kw = self._wgrad("enc.w")
         self._gemm(out, g_op, ws.xp, MN, MN, E, F, M, **kw)
-        K.colsum(g, p["enc.b"].grad, M, E)
 
     def _ln_bwd(self, x, gin, pre, mr, bst, resid, out, out_op, rows, cols, c_total=None, row_reduce=None, bcast=None,
-                moments=True):
+                moments=True, sums=None):
         """Two-phase layer-norm backward + residual add (model.py:242-250): row sums (all-reduced
         over the row group by `row_reduce` when the normalised axis is split), then apply.
         moments=False: the GEMM producing `gin` already accumulated them (JG_EPI_LNB)."""
@@ -514,13 +517,13 @@ class WeatherMixerModel:
         if out_op is not None and out_op is not out and out_op.dtype == torch.float32:
             # fp32 mode: the kernel's operand copy is bf16-only; copy (and push) the fp32 result
             K.ln_bwd_apply(x, gin, p[pre + "gamma"].data, mr, bst, resid, out, None, p[pre + "gamma"].grad,
-                           p[pre + "beta"].grad, rows, cols, c_total)
+                           p[pre + "beta"].grad, rows, cols, c_total, **(sums or {}))
             out_op.view(-1).copy_(out.view(-1))
             for addr in bcast or []:
                 K.copy_async(addr, out, out.numel() * 4)
             return
         K.ln_bwd_apply(x, gin, p[pre + "gamma"].data, mr, bst, resid, out, out_op, p[pre + "gamma"].grad,
-                       p[pre + "beta"].grad, rows, cols, c_total, bcast=bcast)
+                       p[pre + "beta"].grad, rows, cols, c_total, bcast=bcast, **(sums or {}))
 
     # grid paths are implemented in jigsaw_grid.py (bound below)
     def _forward_grid(self, ws):

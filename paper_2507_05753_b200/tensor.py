@@ -318,7 +318,7 @@ def layer_norm_backward(x: torch.Tensor, gamma: torch.Tensor, eps: float, upstre
     dgamma = torch.zeros_like(gamma)
     dbeta = torch.zeros_like(gamma)
     _lib.call("jg_ln_bwd_apply", x.data_ptr(), upstream.data_ptr(), gamma.data_ptr(), mr.data_ptr(),
-              bstats.data_ptr(), None, dx.data_ptr(), None, dgamma.data_ptr(), dbeta.data_ptr(), None,
+              bstats.data_ptr(), None, dx.data_ptr(), None, dgamma.data_ptr(), dbeta.data_ptr(), None, 0, None,
               rows, c, c, None)
     return dx, dgamma, dbeta
 

@@ -263,7 +263,7 @@ def ln_bwd_moments(x, g, gamma, mean_rstd, bstats, rows, cols):
 
 
 def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbeta, rows, cols, c_total,
-                 bcast=None):
+                 bcast=None, rowsum=None, rowsum_period=0, colsum=None):
     mr = mean_rstd.reshape(rows, 2).double()
     xh = (x.reshape(rows, cols).double() - mr[:, :1]) * mr[:, 1:]
     gv = g.reshape(rows, cols).double()
@@ -281,6 +281,10 @@ def ln_bwd_apply(x, g, gamma, mean_rstd, bstats, resid, out, out_op, dgamma, dbe
         dgamma += (gv * xh).sum(0).float()
     if dbeta is not None:
         dbeta += gv.sum(0).float()
+    if rowsum is not None:
+        rowsum += dx.sum(1).reshape(-1, rowsum_period).sum(0).float()
+    if colsum is not None:
+        colsum += dx.sum(0).float()
 
 
 def colsum(x, out, rows, cols, ld=None):
