@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--mp", type=int, default=0,
+                    help="Jigsaw group size (default: all ranks); world / mp data-parallel replicas "
+                         "(groups [k*mp, (k+1)*mp), dp groups r %% mp: SPEC.md:491-499, comm.py:319-361)")
     ap.add_argument("--fused-adam", action="store_true", help="Adam inside the weight-gradient GEMM epilogue")
     return ap.parse_args()
 
@@ -158,7 +161,7 @@ def cpu_reference_sample(cfg_kw, batch):
 
 
 def run_reference(args, rank, world):
-    cfg_kw, lat_real, vars_real, desc = config_for(args.config, world)
+    cfg_kw, lat_real, vars_real, desc = config_for(args.config, args.mp or world)
     if rank != 0:
         return
     from oracle import model as om
@@ -217,9 +220,14 @@ def run_ours(args, rank, world):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     comm = Communicator.from_env()
-    cfg_kw, lat_real, vars_real, desc = config_for(args.config, world)
+    mp = args.mp or world
+    if world % mp:
+        raise SystemExit(f"--mp {mp} does not divide the world size {world}")
+    replicas = world // mp
+    cfg_kw, lat_real, vars_real, desc = config_for(args.config, mp)
     cfg = ModelConfig(**cfg_kw)
-    ctx = MpContext(comm, list(range(world)))
+    base = (rank // mp) * mp
+    ctx = MpContext(comm, list(range(base, base + mp)))
     big = cfg.train_flops() > 1e12
     model = WeatherMixerModel(ctx, cfg, seed=0, dtype=args.dtype, init="fast" if big else "reference")
     model.lat_real, model.vars_real = lat_real, vars_real
@@ -227,7 +235,7 @@ def run_ours(args, rank, world):
     # synthetic z-scored inputs: x, target ~ N(0, 1); padded rows / channels are zero
     lat, lon = model.local_grid
     nv = model.local_vars
-    xd, td = fill_random_inputs(step, lat_real, 1234 + ctx.pos)
+    xd, td = fill_random_inputs(step, lat_real, 1234 + ctx.pos + 7919 * ctx.dp_index)
 
     def barrier():
         if world > 1:
@@ -309,20 +317,22 @@ def run_ours(args, rank, world):
 
     burst, sustained, hbm, peak_kind = peaks()
     flops_step = cfg.train_flops(args.batch)
-    samples_s = args.batch / (ms / 1e3)
-    tflops = flops_step / (ms / 1e3) / 1e12  # FLOPs of one step (all B samples) per second
+    samples_s = args.batch * replicas / (ms / 1e3)  # every replica trains on its own B samples
+    tflops = flops_step * replicas / (ms / 1e3) / 1e12  # FLOPs of one step (all samples) per second
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 / world * world  # per-rank GEMM rate
     line = None
     if rank == 0:
         line = {
             "metric": "WeatherMixer train samples/s", "value": samples_s, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak" if args.config in WEAK else "strong", "vs_baseline": None,
+            "higher_is_better": True,
+            "scaling": "weak" if args.config in WEAK or replicas > 1 else "strong", "vs_baseline": None,
             "dtype": args.dtype,
             "data": "synthetic (x, target ~ N(0,1), ERA5-shaped, random-init weights)",
             "config": {"workload": f"{args.config}: {desc}", "batch": args.batch, "grid_padded": list(cfg.grid),
-                       "tokens": cfg.tokens, "params": model.param_elements() * world,
-                       "parallelism": f"jigsaw {ctx.R}x{ctx.C}" if world > 1 else "single GPU",
+                       "tokens": cfg.tokens, "params": model.param_elements() * mp,
+                       "parallelism": (f"jigsaw {ctx.R}x{ctx.C}" if mp > 1 else "single GPU")
+                                      + (f" x dp{replicas}" if replicas > 1 else ""),
                        "l2": "working set per step >> 126 MB L2 (weights + activations, GB-scale); no flush needed",
                        "loss": float(loss_val)},
             "tflops": tflops, "pct_bf16_peak": 100.0 * tflops / (world * sustained),
@@ -334,7 +344,7 @@ def run_ours(args, rank, world):
                          "launches": len(recs), "gemm_share_of_eager_step": gemm_ms / eager_ms,
                          "peak_basis": f"{peak_kind} sustained bf16 (kernel timed inside a long step)"},
             "clocks": clock,
-            "e2e": {"value": args.batch / (e2e_ms / 1e3), "unit": "samples/s",
+            "e2e": {"value": args.batch * replicas / (e2e_ms / 1e3), "unit": "samples/s",
                     "h2d_bytes_per_step": step.h2d_bytes_per_step * world, "d2h_bytes_per_step": step.d2h_bytes_per_step * world,
                     "ms_per_step": e2e_ms, "device_ms_per_call": e2e_call_ms,
                     "api": "TrainStep.__call__(x_host_pinned, target_host_pinned, prefetch_next=(x, target)) -> float loss",

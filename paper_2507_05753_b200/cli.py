@@ -4,7 +4,7 @@ JSON experiment config.
 
     python -m paper_2507_05753_b200 verify --config exp.json [--out DIR]
     python -m paper_2507_05753_b200 train  --config exp.json --out DIR
-    python -m paper_2507_05753_b200 bench  {strong,roofline} [--config exp.json | --workload C4] --out DIR
+    python -m paper_2507_05753_b200 bench  {strong,roofline,weak,dp} [--workload C4] [--mp 2] --out DIR
     python -m paper_2507_05753_b200 report DIR/strong.csv [...]
     python -m paper_2507_05753_b200 flops  --config exp.json          # count_flops
     python -m paper_2507_05753_b200 co2    E_kWh PUE e_C              # co2_equiv
@@ -258,8 +258,39 @@ def cmd_bench(args) -> int:
             rows.append({"workload": wl, "n": 1, "samples_per_s": d["value"], "tflops": d["tflops"],
                          "gemm_tflops": d["roofline"]["achieved"], "gemm_frac_of_peak": d["roofline"]["frac"],
                          "pct_bf16_peak": d["pct_bf16_peak"]})
+    elif args.suite == "weak":
+        # fixed per-rank work, model grown with n (Table 1 sizing: C5 has n / 2 blocks); weak
+        # efficiency = baseline time / scaled time vs the smallest n
+        workloads = args.workload or ["C5"]
+        for wl in workloads:
+            base = None
+            for n in [m for m in N_WAY if m <= ngpu and (m > 1 or wl != "C5")]:
+                d = _bench_line(n, wl, ["--steps", str(args.steps), "--warmup", str(args.warmup)])
+                base = base or d
+                per_rank = d["config"]["params"] / n
+                rows.append({"workload": wl, "n": n, "samples_per_s": d["value"], "ms_per_step": d["ms_per_step"],
+                             "tflops": d["tflops"], "params": d["config"]["params"],
+                             "params_per_rank": per_rank,
+                             "params_per_rank_vs_base": per_rank / (base["config"]["params"] / base["n_gpus"]),
+                             "efficiency": base["ms_per_step"] / d["ms_per_step"],
+                             "e2e_samples_per_s": d["e2e"]["value"]})
+    elif args.suite == "dp":
+        # dp_weak: one Jigsaw group of --mp ranks replicated over the node, the data grown with the
+        # replica count (groups r % mp, Table 3); efficiency vs the single replica
+        mp = args.mp
+        for wl in workloads:
+            base = None
+            for k in [k for k in (1, 2, 4, 8) if k * mp <= ngpu]:
+                d = _bench_line(k * mp, wl, ["--steps", str(args.steps), "--warmup", str(args.warmup),
+                                             "--mp", str(mp)])
+                base = base or d["value"]
+                rows.append({"workload": wl, "n": k * mp, "mp": mp, "replicas": k, "samples_per_s": d["value"],
+                             "ms_per_step": d["ms_per_step"], "tflops": d["tflops"], "speedup": d["value"] / base,
+                             "efficiency": d["value"] / (k * base), "e2e_samples_per_s": d["e2e"]["value"]})
     else:
-        raise ConfigErrors([f"bench suite {args.suite!r}: only strong and roofline are built"])
+        raise ConfigErrors([f"bench suite {args.suite!r}: unknown"])
+    if not rows:
+        raise ConfigErrors([f"bench suite {args.suite!r}: no GPU count fits this node ({ngpu} GPUs)"])
     path = os.path.join(args.out, f"{args.suite}.csv")
     with open(path, "w", newline="") as fh:
         w = csv.DictWriter(fh, fieldnames=list(rows[0].keys()), quoting=csv.QUOTE_MINIMAL)
@@ -285,8 +316,10 @@ def report(paths) -> str:
         for r in rows:
             v, n = float(r["samples_per_s"]), int(r["n"])
             b = base.get(r["workload"])
-            sp = v / b if b else float("nan")
-            lines.append(f"{r['workload']:10s} {n:3d} {v:10.3f} {sp:8.2f} {sp / n:10.2f}")
+            sp = float(r["speedup"]) if r.get("speedup") else (v / b if b else float("nan"))
+            # weak / dp suites carry their own efficiency definition
+            eff = float(r["efficiency"]) if r.get("efficiency") else sp / n
+            lines.append(f"{r['workload']:10s} {n:3d} {v:10.3f} {sp:8.2f} {eff:10.2f}")
     return "\n".join(lines)
 
 
@@ -305,6 +338,7 @@ def main(argv=None) -> int:
     p.add_argument("--out", required=True)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--mp", type=int, default=2, help="dp suite: Jigsaw group size of each replica")
     p = sub.add_parser("report")
     p.add_argument("csv", nargs="+")
     p = sub.add_parser("flops")

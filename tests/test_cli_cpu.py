@@ -66,3 +66,20 @@ def test_report_speedups(tmp_path):
     lines = text.splitlines()[1:]
     assert lines[0].split()[3] == "1.00"           # speedup(n=1) = 1.00
     assert lines[2].split()[3] == "3.20" and lines[2].split()[4] == "0.80"
+
+
+def test_report_weak_efficiency(tmp_path):
+    # weak suite rows carry baseline_time / scaled_time: equal times -> 1.0
+    p = tmp_path / "weak.csv"
+    with open(p, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["workload", "n", "samples_per_s", "ms_per_step", "efficiency"])
+        w.writerows([["C5", 2, 5.0, 200.0, 1.0], ["C5", 4, 4.0, 250.0, 0.8]])
+    lines = cli.report([str(p)]).splitlines()[1:]
+    assert lines[0].split()[4] == "1.00" and lines[1].split()[4] == "0.80"
+
+
+def test_bench_suite_without_gpus_is_a_config_error(tmp_path):
+    # no GPU count fits a GPU-less host: exit code 2, no bench process launched
+    assert cli.main(["bench", "weak", "--out", str(tmp_path)]) == cli.EXIT_CONFIG
+    assert cli.main(["bench", "dp", "--mp", "2", "--out", str(tmp_path)]) == cli.EXIT_CONFIG
