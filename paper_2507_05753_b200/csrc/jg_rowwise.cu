@@ -257,7 +257,9 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
                                     float inv_ctotal, const Bcast bc) {
   const int64_t c0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
   const int64_t r0 = blockIdx.y * (int64_t)LNB_ROWS;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // row-sum partials of the 8 warps meet in shared memory: one atomic per row per block
+  __shared__ float srow[LNB_ROWS][8];
   // threads past the last column stay (nc = 0) so whole warps reduce the row sums
   const int nc = c0 >= cols ? 0 : (cols - c0 >= 4 ? 4 : static_cast<int>(cols - c0));
   if (nc == 0 && !rowsum_out) return;
@@ -318,7 +320,7 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
 #pragma unroll
         for (int j = 0; j < 4; ++j) rs += j < nc ? ov[j] : 0.f;
         rs = warp_sum(rs);
-        if (lane == 0) atomicAdd(rowsum_out + r % rowsum_period, rs);
+        if (lane == 0) srow[r - r0][warp] = rs;
       }
       if (nc == 0) continue;
       if (v4) {
@@ -342,6 +344,15 @@ __global__ void ln_bwd_apply_kernel(const float* __restrict__ x, const float* __
             }
           }
       }
+    }
+  }
+  if (rowsum_out) {  // uniform over the block: no thread returned early
+    __syncthreads();
+    if (threadIdx.x < r1 - r0) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += srow[threadIdx.x][w];
+      atomicAdd(rowsum_out + (r0 + threadIdx.x) % rowsum_period, s);
     }
   }
 #pragma unroll

@@ -68,3 +68,22 @@ def test_bench_many_blocks_multi_gpu(n):
     assert p.returncode == 0 and lines, p.stdout[-2000:] + p.stderr[-3000:]
     d = json.loads(lines[-1])
     assert d["n_gpus"] == n and d["value"] > 0 and abs(d["config"]["loss"]) < 1e3
+
+
+@pytest.mark.parametrize("n,mp", [(2, 1), (4, 2)])
+def test_bench_dp_replicas(n, mp):
+    """Jigsaw groups of mp ranks replicated over n GPUs (bench.py --mp; dp_reduce over r % mp in
+    the captured step): the whole-job rate counts every replica's samples."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29571", os.path.join(root, "bench.py"), "--gpus", str(n),
+           "--mp", str(mp), "--config", "C2", "--steps", "2", "--warmup", "3"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert p.returncode == 0 and lines, p.stdout[-2000:] + p.stderr[-3000:]
+    d = json.loads(lines[-1])
+    assert d["n_gpus"] == n and d["value"] > 0 and abs(d["config"]["loss"]) < 1e3
+    assert d["config"]["parallelism"].endswith(f"dp{n // mp}") and d["scaling"] == "weak"
+    assert abs(d["value"] - (n // mp) * 1000.0 / d["ms_per_step"]) < 1e-6 * d["value"]

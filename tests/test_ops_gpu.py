@@ -157,3 +157,26 @@ def test_epilogue_and_ln_kernels_tile_shapes(cuda):
     assert rel_err(out.cpu().numpy(), dx.cpu().numpy()) < 1e-4
     assert rel_err(dg.cpu().numpy(), (gin.double() * xh).sum(0).cpu().numpy()) < 1e-4
     assert rel_err(db.cpu().numpy(), gin.double().sum(0).cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("rows,cols,period", [(130, 1030, 65), (600, 2160, 300), (16380, 4320, 16380)])
+def test_ln_bwd_apply_fused_bias_sums(cuda, rows, cols, period):
+    """Layer-norm backward with the fused bias-gradient sums (row sums folded by r % period for
+    the tok2 row bias, column sums for ch2 / encoder): same results as the exact torch double."""
+    import cpu_kernels as CK
+    from paper_2507_05753_b200 import kernels as K
+    g = torch.Generator(device=cuda).manual_seed(rows + cols)
+    r = lambda *s: torch.randn(*s, device=cuda, generator=g)  # noqa: E731
+    x, gin, resid, gam = r(rows, cols), r(rows, cols), r(rows, cols), r(cols)
+    mr = torch.stack([x.mean(1), 1 / torch.sqrt(x.var(1, unbiased=False) + 1e-5)], 1).contiguous()
+    bst = r(rows, 2)
+    outs = []
+    for impl in (K, CK):
+        out = torch.empty(rows, cols, device=cuda)
+        dg, db = torch.zeros(cols, device=cuda), torch.zeros(cols, device=cuda)
+        rs, cs = torch.full((period,), 0.5, device=cuda), torch.zeros(cols, device=cuda)
+        impl.ln_bwd_apply(x, gin, gam, mr, bst, resid, out, None, dg, db, rows, cols, cols,
+                          rowsum=rs, rowsum_period=period, colsum=cs)
+        outs.append((out, dg, db, rs, cs))
+    for a, b in zip(*outs):
+        assert rel_err(a.double().cpu().numpy(), b.double().cpu().numpy()) < 1e-4

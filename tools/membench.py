@@ -92,6 +92,11 @@ resid = rnd(M, El)
 dg, db = torch.zeros(El, device=dev), torch.zeros(El, device=dev)
 run("ln_bwd_apply", lambda: K.ln_bwd_apply(res, gin, gam, mr, bst, resid, out, out_op, dg, db, M, El, E),
     M * El * (4 + 4 + 4 + 4 + 2))
+rsb, csb = torch.zeros(Tl, device=dev), torch.zeros(El, device=dev)
+run("ln_bwd_apply_rowsum", lambda: K.ln_bwd_apply(res, gin, gam, mr, bst, resid, out, out_op, dg, db, M, El, E,
+                                                  rowsum=rsb, rowsum_period=Tl), M * El * (4 + 4 + 4 + 4 + 2))
+run("ln_bwd_apply_colsum", lambda: K.ln_bwd_apply(res, gin, gam, mr, bst, resid, out, out_op, dg, db, M, El, E,
+                                                  colsum=csb), M * El * (4 + 4 + 4 + 4 + 2))
 
 # bias gradients
 gc = rnd(M, H // C, dtype=bf)
