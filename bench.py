@@ -319,7 +319,7 @@ def run_ours(args, rank, world):
     flops_step = cfg.train_flops(args.batch)
     samples_s = args.batch * replicas / (ms / 1e3)  # every replica trains on its own B samples
     tflops = flops_step * replicas / (ms / 1e3) / 1e12  # FLOPs of one step (all samples) per second
-    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 / world * world  # per-rank GEMM rate
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12  # this rank's GEMM rate (rank 0's launches)
     line = None
     if rank == 0:
         line = {
