@@ -23,6 +23,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr",
     f"-I{ROOT / 'include'}",
+    *os.environ.get("JG_NVCC_EXTRA", "").split(),  # experiment-only defines (e.g. -DJG_TILE_GROUP_M=16)
 ]
 
 

@@ -243,7 +243,10 @@ __device__ __forceinline__ void stage_store(uint8_t* stg, const float* v, bool b
 // L2-aware tile order: tiles run m-fastest inside groups of TILE_GROUP_M row tiles, so one wave of
 // ~148 CTAs covers a ~8 x (units/8) block of the output and reads ~8 + units/8 operand panels per
 // k-step from DRAM instead of (units / n_tiles) + n_tiles (long-K token GEMMs: B re-read per wave).
-constexpr int TILE_GROUP_M = 8;
+#ifndef JG_TILE_GROUP_M
+#define JG_TILE_GROUP_M 8
+#endif
+constexpr int TILE_GROUP_M = JG_TILE_GROUP_M;
 __device__ __forceinline__ void tile_coords(int rem, int m_tiles, int n_tiles, int& mi, int& ni) {
   const int per_group = TILE_GROUP_M * n_tiles;
   const int g = rem / per_group;
