@@ -9,9 +9,8 @@ synthetic ERA5-shaped sample (B = 1) of the chosen config; N > 1 runs Jigsaw ove
 grid of N GPUs (strong scaling: the global model and batch are fixed). Launched with
 torchrun for N > 1; rank 0 prints one JSON line.
 
-`--impl reference` times the reference algorithm on the host cores instead (the numpy port
-in oracle/, kind "port": the reference is pure Python, so nothing compiles into oracle/_ref),
-on a bounded sample (one mixer block fwd+bwd at full shape, extrapolated by FLOPs).
+`--impl reference` times full training steps of the unmodified reference package (pure numpy,
+installed in baseline/_ref) on the host cores instead; see baseline/reference_step.py.
 """
 from __future__ import annotations
 
@@ -151,44 +150,72 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_reference_sample(cfg_kw, batch):
-    """(samples/s, cores, sample description, seconds per full step) from the oracle port."""
+def cpu_reference_sample(cfg_kw, lat_real, vars_real, batch):
+    """Bounded CPU baseline (rank 0, N = 1): ONE training step of the unmodified reference
+    (baseline/_ref, f32, all host cores; baseline/reference_step.py) on the same config with
+    ONE mixer block, extrapolated to the full depth by FLOPs (the blocks carry >= 90 % of the
+    step's FLOPs at C4). Falls back to the oracle port's block sample when the reference is
+    not installed. Returns the cpu_baseline dict."""
+    from baseline import reference_step as rsm
+    cores = rsm.host_cores()
+    if rsm.load_reference() is not None:
+        from oracle import model as om
+        one = dict(cfg_kw, n_blocks=1)
+        times, _, init_s, _, rs = rsm.time_steps(one, lat_real, vars_real, batch, warmup=0, steps=1, budget_s=60)
+        full = om.Config(**{k: v for k, v in cfg_kw.items() if k != "dropout_rate"})
+        scale = om.train_flops(full, batch) / rs.flops()
+        t_step = times[0] * scale
+        return {"value": batch / t_step, "unit": "samples/s", "cores": cores, "kind": "reference",
+                "sample": f"one training step (zero_grads, forward, SPEC loss, backward, grad_sync, Adam) of the "
+                          f"unmodified reference package (baseline/_ref, f32 numpy/OpenBLAS, {cores} threads, "
+                          f"{rsm.cpu_model()}) at the full config with 1 of {cfg_kw['n_blocks']} blocks: "
+                          f"{times[0]:.2f} s, x{scale:.2f} by FLOPs -> {t_step:.1f} s per step"}
     from oracle import model as om
     from oracle.cpu_baseline import step_estimate
     oc = om.Config(**{k: v for k, v in cfg_kw.items() if k != "dropout_rate"})
     t_step, t_block, cores = step_estimate(oc, batch)
-    return batch / t_step, cores, t_block, t_step
+    return {"value": batch / t_step, "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"one mixer block fwd+bwd at full shape (oracle port, f32 numpy/OpenBLAS), {t_block:.2f} s, "
+                      f"extrapolated by FLOPs to {t_step:.1f} s per step"}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: full training steps of the UNMODIFIED reference package on the host
+    cores (baseline/reference_step.py), rank 0 only. A C4 step takes ~0.5 min on 16 cores, so
+    the warm-up and timed steps are capped to fit REF_BUDGET_S; the line reports the counts
+    actually run (steps x ms_per_step is the timed work)."""
     cfg_kw, lat_real, vars_real, desc = config_for(args.config, args.mp or world)
     if rank != 0:
         return
+    from baseline import reference_step as rsm
+    if rsm.load_reference() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "reference package not installed in baseline/_ref"}))
+        return
     from oracle import model as om
-    from oracle.cpu_baseline import block_flops, time_block
-    oc = om.Config(**cfg_kw)
-    t_first = time_block(oc, args.batch, repeats=1)
-    budget = 200.0  # seconds of CPU work for the whole reference run
-    per = max(t_first, 1e-6)
-    warm = min(args.warmup, max(0, int(budget * 0.2 / per)))
-    steps = max(1, min(args.steps, int(budget / per)))
-    for _ in range(warm):
-        time_block(oc, args.batch, repeats=0) if False else None  # the first call above already warmed
-    times = [time_block(oc, args.batch, repeats=1) for _ in range(steps)]
-    t_block = statistics.median(times)
-    scale = om.train_flops(oc, args.batch) / block_flops(oc, args.batch)
-    t_step = t_block * scale
+    budget = float(os.environ.get("REF_BUDGET_S", "150"))
+    times, warm, init_s, loss, rs = rsm.time_steps(cfg_kw, lat_real, vars_real, args.batch, args.warmup,
+                                                   args.steps, budget)
+    t_step = statistics.median(times)
     value = args.batch / t_step
-    cores = os.cpu_count()
-    sample = (f"one mixer block fwd+bwd at full {args.config} shape, f32 numpy/OpenBLAS ({cores} threads), "
-              f"median of {steps} x {t_block:.2f} s, extrapolated x{scale:.2f} by FLOPs to the full step")
+    cores = rsm.host_cores()
+    oc = om.Config(**{k: v for k, v in cfg_kw.items() if k != "dropout_rate"})
+    flops = om.train_flops(oc, args.batch)
+    sample = (f"full training steps of the unmodified reference package (baseline/_ref jigsaw 0.1.0, n = 1, f32 "
+              f"numpy/OpenBLAS on {cores} threads, {rsm.cpu_model()}): zero_grads, forward, SPEC loss, backward, "
+              f"grad_sync, Adam; {warm} warm-up + {len(times)} timed steps (median {t_step:.2f} s; capped to "
+              f"{budget:.0f} s of work, requested --warmup {args.warmup} --steps {args.steps}); init {init_s:.1f} s "
+              f"untimed")
     line = {
         "impl": "reference", "metric": "WeatherMixer train samples/s", "value": value, "unit": "samples/s",
-        "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {desc}", "batch": args.batch, "parallelism": "cpu (reference algorithm)"},
-        "tflops": om.train_flops(oc, args.batch) / t_step / 1e12,
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+        "n_gpus": world, "steps": len(times), "warmup": warm, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (x, target ~ N(0,1), padded rows / channels zero)",
+        "config": {"workload": f"{args.config}: {desc}", "batch": args.batch,
+                   "parallelism": "host CPU, reference n = 1 (its fastest configuration on one host)",
+                   "loss": loss},
+        "tflops": flops / t_step / 1e12, "counted_flops_per_step": rs.flops() // max(1, len(times) + warm),
+        "step_times_s": times,
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -229,8 +256,8 @@ def run_ours(args, rank, world):
     base = (rank // mp) * mp
     ctx = MpContext(comm, list(range(base, base + mp)))
     big = cfg.train_flops() > 1e12
-    model = WeatherMixerModel(ctx, cfg, seed=0, dtype=args.dtype, init="fast" if big else "reference")
-    model.lat_real, model.vars_real = lat_real, vars_real
+    model = WeatherMixerModel(ctx, cfg, seed=0, dtype=args.dtype, init="fast" if big else "reference",
+                              lat_real=lat_real, vars_real=vars_real)
     step = TrainStep(model, batch=args.batch, graph=not args.no_graph, fused_adam=args.fused_adam)
     # synthetic z-scored inputs: x, target ~ N(0, 1); padded rows / channels are zero
     lat, lon = model.local_grid
@@ -357,11 +384,7 @@ def run_ours(args, rank, world):
         }
     # CPU baseline: rank 0, N = 1 only
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, t_block, t_step = cpu_reference_sample(cfg_kw, args.batch)
-        line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-                                "sample": f"one mixer block fwd+bwd at full {args.config} shape on the host, "
-                                          f"f32 numpy/OpenBLAS, {t_block:.2f} s, extrapolated by FLOPs to "
-                                          f"{t_step:.1f} s per step"}
+        line["cpu_baseline"] = cpu_reference_sample(cfg_kw, lat_real, vars_real, args.batch)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -11,6 +11,8 @@ from .comm import Communicator, ProcessGroup
 from .config import ModelConfig
 from .errors import CommError, CommTimeout, ConfigError, ShapeError, WorkerError
 from .model import Layout, WeatherMixerModel
+from .layers import MixerBlock, ShardedLayerNorm, ShardedLinear
+from .params import Param
 from .parallel import MpContext, comm_volume, pnn, pnt, ptn
 from .sharding import ShardSpec, gather, shard
 from .tensor import MatmulMode
@@ -20,6 +22,7 @@ from .engine import Trainer, TrainStep
 from . import checkpoint
 
 __all__ = [
+    "MixerBlock", "Param", "ShardedLayerNorm", "ShardedLinear",
     "Communicator", "CommError", "CommTimeout", "ConfigError", "Layout", "MatmulMode", "ModelConfig",
     "MpContext", "ProcessGroup", "ShapeError", "ShardSpec", "WeatherMixerModel", "WorkerError",
     "comm_volume", "gather", "pnn", "pnt", "ptn", "shard",

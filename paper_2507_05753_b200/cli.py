@@ -190,9 +190,11 @@ def cmd_train(args) -> int:
         lat, lon = model_cfg.grid
         src = np.random.default_rng(int(cfg.get("seed", 0))).standard_normal(
             (int(data.get("synthetic", 8)) + lead, lat, lon, model_cfg.n_vars)).astype(np.float32)
-    model = WeatherMixerModel(ctx, model_cfg, seed=int(cfg.get("seed", 0)), dtype=cfg.get("dtype", "bf16"))
     loader = TileLoader(src, model_cfg, ctx, lead=max(lead, int(run.get("r_max", 1))), batch=int(run.get("batch", 1)),
                         seed=int(run.get("seed", 0)))
+    # padded rows / channels of the source weigh 0 in the loss
+    model = WeatherMixerModel(ctx, model_cfg, seed=int(cfg.get("seed", 0)), dtype=cfg.get("dtype", "bf16"),
+                              lat_real=loader.lat_real, vars_real=loader.vars_real)
     trainer = Trainer(model, batch=int(run.get("batch", 1)), adam=adam, r_max=int(run.get("r_max", 1)),
                       seed=int(run.get("seed", 0)))
     rows, steps_left = [], int(run.get("steps", loader.steps_per_epoch()))

@@ -27,8 +27,20 @@ FLAGS = [
 ]
 
 
+STAMP = PKG / ".libjigsaw_sm100.flags"  # the flags the in-tree .so was built with
+
+
+def _flags_id() -> str:
+    return " ".join(FLAGS + SOURCES)
+
+
 def _stale() -> bool:
     if not OUT.exists():
+        return True
+    try:
+        if STAMP.read_text() != _flags_id():
+            return True  # built with other flags (e.g. an experiment's JG_NVCC_EXTRA)
+    except OSError:
         return True
     t = OUT.stat().st_mtime
     deps = [HERE / s for s in SOURCES] + list(HERE.glob("*.cuh")) + [ROOT / "include" / "jigsaw_sm100.h", Path(__file__)]
@@ -51,6 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs, "-lcudart"],
                    check=True)
     os.replace(tmp, OUT)
+    STAMP.write_text(_flags_id())
     for o in objs:
         os.unlink(o)
     return OUT

@@ -339,6 +339,10 @@ class Trainer:
         and rollouts, and the wall time."""
         import time
         nb = loader.steps_per_epoch() if max_steps is None else min(max_steps, loader.steps_per_epoch())
+        if (loader.lat_real, loader.vars_real) != (self.model.lat_real, self.model.vars_real):
+            raise ConfigError(f"loader data is {loader.lat_real} rows x {loader.vars_real} channels but the model's "
+                              f"loss mask is {self.model.lat_real} x {self.model.vars_real}: build the model with "
+                              f"lat_real=loader.lat_real, vars_real=loader.vars_real")
         rs = self.draw_rollouts(nb)
         if self.r_max > 1 and loader.lead < self.r_max:
             raise ConfigError(f"loader lead {loader.lead} < r_max {self.r_max}: build it with lead=r_max")

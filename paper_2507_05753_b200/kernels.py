@@ -75,6 +75,16 @@ def patchify(x, tok, batch, lat, lon, chans, pl, pw):
     _lib.call("jg_patchify", x.data_ptr(), tok.data_ptr(), _lib.dtype_code(tok), batch, lat, lon, chans, pl, pw)
 
 
+def gelu_fwd(x, y):
+    """y = x * Phi(x), exact erf (reference tensor.py:75-77)."""
+    _lib.call("jg_gelu_fwd", x.data_ptr(), y.data_ptr(), _lib.dtype_code(x), x.numel())
+
+
+def gelu_bwd(x, g, dx):
+    """dx = g * (Phi(x) + x phi(x)) (reference tensor.py:80-84)."""
+    _lib.call("jg_gelu_bwd", x.data_ptr(), g.data_ptr(), dx.data_ptr(), _lib.dtype_code(x), x.numel())
+
+
 def ln_moments(x, stats, rows, cols):
     _lib.call("jg_ln_moments", x.data_ptr(), stats.data_ptr(), rows, cols, cols)
 

@@ -131,7 +131,11 @@ class WeatherMixerModel:
     """Encoder, mixing-block stack, decoder and blend over local Jigsaw tiles (model.py:300-529)."""
 
     def __init__(self, ctx: MpContext, cfg: ModelConfig, seed: int = 0, dtype: str = "bf16",
-                 eps: float = 1e-5, init: str = "reference", device=None):
+                 eps: float = 1e-5, init: str = "reference", device=None, *, lat_real: int | None = None,
+                 vars_real: int | None = None):
+        """lat_real / vars_real: rows and channels of the unpadded data (e.g. 721 of 728 rows, 69 of
+        70 channels at 0.25 deg). The loss gives padded rows / channels weight 0 and averages over
+        B x lat_real x lon x vars_real. Default: nothing padded."""
         cfg.validate(ctx.n)
         if dtype not in DTYPES:
             raise ShapeError(f"dtype {dtype!r} not supported on sm_100a (use 'bf16' or 'f32'; f64 lives in oracle/)")
@@ -140,6 +144,11 @@ class WeatherMixerModel:
         if eps <= 0:
             raise ValueError(f"layer_norm eps must be > 0, got {eps}")
         self.ctx, self.cfg, self.seed, self.eps = ctx, cfg, seed, eps
+        self.lat_real = cfg.grid[0] if lat_real is None else int(lat_real)
+        self.vars_real = cfg.n_vars if vars_real is None else int(vars_real)
+        if not (1 <= self.lat_real <= cfg.grid[0] and 1 <= self.vars_real <= cfg.n_vars):
+            raise ConfigError(f"lat_real {self.lat_real} / vars_real {self.vars_real} outside the padded grid "
+                              f"{cfg.grid[0]} rows x {cfg.n_vars} channels")
         self.dtype_name = dtype
         self.op_dtype = DTYPES[dtype]
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -244,6 +253,50 @@ class WeatherMixerModel:
         if self.flat.op is not self.flat.master:
             K.cast_bf16(self.flat.master, self.flat.op)
         self.weights_version = getattr(self, "weights_version", 0) + 1
+
+    # -- reference layer objects (model.py:336-389) -----------------------------------------
+    def _layer_objects(self) -> dict:
+        """encoder / blocks / decoder / blend as the reference exposes them: layer objects of
+        layers.py over this model's Params (one op at a time; the training step instead runs
+        the fused schedule below over the same Params)."""
+        if getattr(self, "_layer_objs", None) is None:
+            from .layers import MixerBlock, ShardedLayerNorm, ShardedLinear
+            from .tensor import MatmulMode
+            p, ctx, E = self.params, self.ctx, self.cfg.d_emb
+
+            def ln(pre):
+                return ShardedLayerNorm(ctx, p[pre + "gamma"], p[pre + "beta"], E, self.eps, out_dtype=self.op_dtype)
+
+            blocks = []
+            for i in range(self.cfg.n_blocks):
+                b = f"block{i}."
+                blocks.append(MixerBlock(
+                    ctx, ln(b + "ln1."), ShardedLinear(ctx, p[b + "tok1.w"], p[b + "tok1.b"], MatmulMode.TN),
+                    ShardedLinear(ctx, p[b + "tok2.w"], p[b + "tok2.b"], MatmulMode.NT, weight_first=True),
+                    ln(b + "ln2."), ShardedLinear(ctx, p[b + "ch1.w"], p[b + "ch1.b"], MatmulMode.NT),
+                    ShardedLinear(ctx, p[b + "ch2.w"], p[b + "ch2.b"], MatmulMode.NT), self.cfg.dropout_rate))
+            self._layer_objs = {
+                "encoder": ShardedLinear(ctx, p["enc.w"], p["enc.b"], MatmulMode.NT),
+                "blocks": blocks,
+                "decoder": ShardedLinear(ctx, p["dec.w"], p["dec.b"], MatmulMode.NT),
+            }
+        return self._layer_objs
+
+    @property
+    def encoder(self):
+        return self._layer_objects()["encoder"]
+
+    @property
+    def blocks(self):
+        return self._layer_objects()["blocks"]
+
+    @property
+    def decoder(self):
+        return self._layer_objects()["decoder"]
+
+    @property
+    def blend(self) -> Param:
+        return self.params["blend.w"]
 
     # -- introspection (model.py:462-529) -------------------------------------------------
     @property
@@ -594,8 +647,7 @@ class _Workspace:
         self.gu = torch.empty((B, Tl, El), **f32)
         # loss weights over the local grid block (padded rows / channels weigh 0)
         from .train import lat_weights, var_weights
-        lat_real = getattr(model, "lat_real", lat)
-        vars_real = getattr(model, "vars_real", cfg.n_vars)
+        lat_real, vars_real = model.lat_real, model.vars_real
         self.lat_w = torch.tensor(lat_weights(lat, lat_real), **f32)
         vw = var_weights(cfg.n_vars, vars_real)
         c0 = model.sets["V_C"][model.c][0] if C > 1 else 0

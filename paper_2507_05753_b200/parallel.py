@@ -96,6 +96,14 @@ class MpContext:
     def _count(self, m: int, n: int, k: int, batch: int = 1) -> None:
         self.flops += 2 * m * n * k * batch
 
+    def _buf_acquire(self, size: int) -> None:
+        """Live communication buffers holding parameter blocks, and their watermark (parallel.py:71-76)."""
+        self.param_buffer_elements += size
+        self.param_buffer_peak = max(self.param_buffer_peak, self.param_buffer_elements)
+
+    def _buf_release(self, size: int) -> None:
+        self.param_buffer_elements -= size
+
     # -- collectives on the grid axes (device tensors, current stream) --------
     def all_gather_row(self, x: torch.Tensor) -> torch.Tensor:
         """[C, *x.shape] stack of the row group's blocks (ordered by column index)."""
@@ -103,7 +111,7 @@ class MpContext:
         if self.C == 1:
             out[0].copy_(x)
         else:
-            dist.all_gather_into_tensor(out, x.contiguous(), group=self.row_group)
+            dist.all_gather_into_tensor(out.view(-1), x.contiguous().view(-1), group=self.row_group)
         return out
 
     def all_gather_col(self, x: torch.Tensor) -> torch.Tensor:
@@ -111,7 +119,7 @@ class MpContext:
         if self.R == 1:
             out[0].copy_(x)
         else:
-            dist.all_gather_into_tensor(out, x.contiguous(), group=self.col_group)
+            dist.all_gather_into_tensor(out.view(-1), x.contiguous().view(-1), group=self.col_group)
         return out
 
     def reduce_scatter_row(self, planes: torch.Tensor) -> torch.Tensor:
@@ -119,14 +127,14 @@ class MpContext:
         if self.C == 1:
             return planes[0]
         out = torch.empty(planes.shape[1:], dtype=planes.dtype, device=planes.device)
-        dist.reduce_scatter_tensor(out, planes.contiguous(), group=self.row_group)
+        dist.reduce_scatter_tensor(out.view(-1), planes.contiguous().view(-1), group=self.row_group)
         return out
 
     def reduce_scatter_col(self, planes: torch.Tensor) -> torch.Tensor:
         if self.R == 1:
             return planes[0]
         out = torch.empty(planes.shape[1:], dtype=planes.dtype, device=planes.device)
-        dist.reduce_scatter_tensor(out, planes.contiguous(), group=self.col_group)
+        dist.reduce_scatter_tensor(out.view(-1), planes.contiguous().view(-1), group=self.col_group)
         return out
 
     # -- into pre-allocated outputs (graph-capture friendly; used by the fused model path) --
@@ -188,65 +196,114 @@ def _split_even(size: int, parts: int, what: str) -> int:
     return size // parts
 
 
+def _gather_axis(blocks: torch.Tensor, axis: int) -> torch.Tensor:
+    """[G, *shape] stack of gathered blocks -> one tensor concatenated along `axis` (< 0) of shape."""
+    g = blocks.shape[0]
+    moved = blocks.movedim(0, blocks.dim() + axis - 1)  # G just before the target axis
+    shape = list(blocks.shape[1:])
+    shape[axis] *= g
+    return moved.reshape(shape)
+
+
+def _lead_pad(t: torch.Tensor, lead: int) -> torch.Tensor:
+    """View with `lead` leading batch dims (singletons prepended) so plane-batched operands broadcast."""
+    return t.reshape((1,) * (lead - (t.dim() - 2)) + tuple(t.shape))
+
+
+def _count_out(ctx: MpContext, out_shape, k: int) -> None:
+    """The reference's FLOP counter: 2 * out.size * k per local GEMM (parallel.py:65-69)."""
+    n = 1
+    for s in out_shape:
+        n *= int(s)
+    ctx.flops += 2 * n * int(k)
+
+
+def _param_blocks(ctx: MpContext, gathered: torch.Tensor, own: torch.Tensor, is_param: bool):
+    """Account received parameter blocks in the buffer watermark (parallel.py:71-76, 79-97)."""
+    if is_param:
+        ctx._buf_acquire(gathered.numel() - own.numel())
+    return gathered.numel() - own.numel() if is_param else 0
+
+
 def pnt(ctx: MpContext, a: torch.Tensor, b: torch.Tensor, *, a_is_param: bool = False,
         b_is_param: bool = False) -> torch.Tensor:
     """Collective C = A B^T on block operands (parallel.py:107-116).
 
-    Rank (r, c) holds A(r, c) [..., m/R, k/C] and B(r, c) [n/R, k/C] (trailing two dims;
-    n = 2 splits only the last dim) and returns C(r, c) [..., m/R, n/C].
+    Rank (r, c) of the R x C grid holds A(r, c) [..., m/R, k/C] and B(r, c) [..., n/R, k/C] and
+    returns C(r, c) [..., m/R, n/C] — for n = 2 (1 x 2) and n = 4 (2 x 2) exactly the reference's
+    column-block / 2 x 2-block layouts (parallel.py:1-10). Schedule: all-gather B over the
+    column group (B(:, c), all n rows), one local GEMM per output plane (partials over k/C),
+    reduce-scatter the planes over the row group; every rank does 1/n of the FLOPs.
     """
     _check_dtypes("pnt", a, b)
     if ctx.n == 1:
         out = T.matmul(a, b, MatmulMode.NT)
-        ctx._count(out.shape[-2], out.shape[-1], a.shape[-1], out[..., 0, 0].numel())
+        _count_out(ctx, out.shape, a.shape[-1])
         return out
-    # gather B's rows (all n) for this column block
-    b_col = ctx.all_gather_col(b)                          # [R, n/R, k/C]
-    b_panel = b_col.reshape(-1, b.shape[-1])               # [n, k/C]
-    n_total = b_panel.shape[0]
-    _split_even(n_total, ctx.C, "pnt output dimension")
-    part = T.matmul(a, b_panel, MatmulMode.NT)             # [..., m/R, n] partial over k/C
-    ctx._count(part.shape[-2], part.shape[-1], a.shape[-1], part[..., 0, 0].numel())
-    planes = torch.stack(part.split(n_total // ctx.C, dim=-1))  # [C, ..., m/R, n/C]
-    return ctx.reduce_scatter_row(planes)
+    held = 0
+    try:
+        panel = _gather_axis(ctx.all_gather_col(b), -2) if ctx.R > 1 else b   # [..., n, k/C]
+        held = _param_blocks(ctx, panel, b, b_is_param)
+        n_c = _split_even(panel.shape[-2], ctx.C, "pnt output dimension")
+        # planes [C, ..., m/R, n/C]: plane j = A B_panel[j-th n chunk]^T (broadcast batch, no copies)
+        lead = max(a.dim(), panel.dim()) - 2
+        pl = _lead_pad(panel, lead)
+        bp = pl.reshape(*pl.shape[:-2], ctx.C, n_c, pl.shape[-1]).movedim(-3, 0)
+        planes = T.matmul(_lead_pad(a, lead).unsqueeze(0), bp, MatmulMode.NT)
+        _count_out(ctx, planes.shape, a.shape[-1])
+        return ctx.reduce_scatter_row(planes)
+    finally:
+        ctx._buf_release(held)
 
 
 def pnn(ctx: MpContext, a: torch.Tensor, b: torch.Tensor, *, a_is_param: bool = False,
         b_is_param: bool = False) -> torch.Tensor:
-    """Collective C = A B (parallel.py:189-198): rank holds A(r,c) [m/R, k/C], B(r,c) [k/R, n/C]."""
+    """Collective C = A B (parallel.py:189-198): rank holds A(r, c) [..., m/R, k/C] and
+    B(r, c) [..., k/R, n/C], returns C(r, c) [..., m/R, n/C]. Schedule: all-gather A over the
+    row group (all k columns) and B over the column group (all k rows), one local GEMM."""
     _check_dtypes("pnn", a, b)
     if ctx.n == 1:
         out = T.matmul(a, b, MatmulMode.NN)
-        ctx._count(out.shape[-2], out.shape[-1], a.shape[-1], out[..., 0, 0].numel())
+        _count_out(ctx, out.shape, a.shape[-1])
         return out
-    # A B = A (B^T)^T: transpose-gather B so the column split of the product is over n.
-    # Gather B over the column group -> B(:, c) = rows k (all), cols n/C (this column block).
-    b_full_k = ctx.all_gather_col(b).reshape(-1, b.shape[-1])      # [k, n/C]
-    # A's k-columns are split over the row group: gather them -> A(r, :) [m/R, k]
-    a_row = ctx.all_gather_row(a)                                    # [C, ..., m/R, k/C]
-    a_full = torch.cat(list(a_row), dim=-1)                          # [..., m/R, k]
-    out = T.matmul(a_full, b_full_k, MatmulMode.NN)
-    ctx._count(out.shape[-2], out.shape[-1], a_full.shape[-1], out[..., 0, 0].numel())
-    return out
+    held = 0
+    try:
+        b_full = _gather_axis(ctx.all_gather_col(b), -2) if ctx.R > 1 else b   # [..., k, n/C]
+        held += _param_blocks(ctx, b_full, b, b_is_param)
+        a_full = _gather_axis(ctx.all_gather_row(a), -1) if ctx.C > 1 else a   # [..., m/R, k]
+        held += _param_blocks(ctx, a_full, a, a_is_param)
+        out = T.matmul(a_full, b_full, MatmulMode.NN)
+        _count_out(ctx, out.shape, a_full.shape[-1])
+        return out
+    finally:
+        ctx._buf_release(held)
 
 
 def ptn(ctx: MpContext, a: torch.Tensor, b: torch.Tensor, *, a_is_param: bool = False,
         b_is_param: bool = False) -> torch.Tensor:
-    """Collective C = A^T B (parallel.py:276-285): rank holds A(r,c) [p/R, q/C], B(r,c) [p/R, s/C];
-    returns C(r, c) [q/R, s/C]."""
+    """Collective C = A^T B (parallel.py:276-285): rank holds A(r, c) [..., p/R, q/C] and
+    B(r, c) [..., p/R, s/C], returns C(r, c) [..., q/R, s/C] (n = 2: the two q halves stacked,
+    as _tn2). Schedule: all-gather A over the row group (all q columns), one local GEMM per
+    output plane (partials over p/R), reduce-scatter the planes over the column group."""
     _check_dtypes("ptn", a, b)
     if ctx.n == 1:
         out = T.matmul(a, b, MatmulMode.TN)
-        ctx._count(out.shape[-2], out.shape[-1], a.shape[-2], out[..., 0, 0].numel())
+        _count_out(ctx, out.shape, a.shape[-2])
         return out
-    a_row = ctx.all_gather_row(a)                                    # [C, ..., p/R, q/C]
-    a_full = torch.cat(list(a_row), dim=-1)                          # [..., p/R, q]
-    part = T.matmul(a_full, b, MatmulMode.TN)                        # [..., q, s/C] partial over p/R
-    ctx._count(part.shape[-2], part.shape[-1], a_full.shape[-2], part[..., 0, 0].numel())
-    q = part.shape[-2]
-    _split_even(q, ctx.R, "ptn output rows")
-    planes = torch.stack(part.split(q // ctx.R, dim=-2))            # [R, ..., q/R, s/C]
-    return ctx.reduce_scatter_col(planes)
+    held = 0
+    try:
+        a_full = _gather_axis(ctx.all_gather_row(a), -1) if ctx.C > 1 else a   # [..., p/R, q]
+        held = _param_blocks(ctx, a_full, a, a_is_param)
+        q_r = _split_even(a_full.shape[-1], ctx.R, "ptn output rows")
+        # planes [R, ..., q/R, s/C]: plane i = A_full[:, i-th q chunk]^T B
+        lead = max(a_full.dim(), b.dim()) - 2
+        af = _lead_pad(a_full, lead)
+        ap = af.reshape(*af.shape[:-1], ctx.R, q_r).movedim(-2, 0)
+        planes = T.matmul(ap, _lead_pad(b, lead).unsqueeze(0), MatmulMode.TN)
+        _count_out(ctx, planes.shape, a_full.shape[-2])
+        return ctx.reduce_scatter_col(planes)
+    finally:
+        ctx._buf_release(held)
 
 
 PRIMITIVES = {MatmulMode.NT: pnt, MatmulMode.NN: pnn, MatmulMode.TN: ptn}

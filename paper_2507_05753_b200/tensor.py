@@ -30,6 +30,16 @@ DTYPES = {"f32": torch.float32, "bf16": torch.bfloat16}
 # set; bytes = operands read once + output written once (+ read when accumulating).
 GEMM_TIMER: list | None = None
 
+# 3xTF32 K-chunking (fp32 mode). tcgen05's fp32 accumulation of each MMA step is not
+# round-to-nearest: its error grows ~ K^1.5 (relative ~1.3e-8 * K measured on B200,
+# tools/f32_diag.py: 2e-6 at K = 64, 2.2e-4 at K = 16380). fp32-mode GEMMs with K above
+# TF32X3_KCHUNK therefore accumulate K-chunks into separate fp32 planes that jg_epilogue sums
+# (round-to-nearest) before the real epilogue: ~7e-6 per GEMM at 512. bf16 mode is unaffected
+# (its operand rounding, 2^-9, dominates).
+import os as _os  # noqa: E402
+
+TF32X3_KCHUNK = int(_os.environ.get("JG_TF32X3_KCHUNK", "512"))
+
 
 class MatmulMode(str, enum.Enum):
     """The three layer multiplication layouts: X@W, X@W.T and X.T@W (tensor.py:27-33)."""
@@ -98,6 +108,12 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
         b, b_lo, b_bs = split_operand(b, b_major, n, k, batch, b_bs, ldb)
         a_major = b_major = _lib.JG_KMAJOR
         lda = ldb = a.shape[-1]
+    if (fp32 and TF32X3_KCHUNK > 0 and k > TF32X3_KCHUNK and adam is None and d_planes is None and rs is None
+            and d_bcast is None and d2_bcast is None and a_major == _lib.JG_KMAJOR and b_major == _lib.JG_KMAJOR):
+        return _gemm_tf32x3_chunked(out, a, a_lo, b, b_lo, m, n, k, batch, a_bs, b_bs, lda, ldb, reduce_batch,
+                                    dict(epi=epi, alpha=alpha, d2=d2, bias=bias, bias_bs=bias_bs, resid=resid, r_bs=r_bs,
+                                         pre=pre, p_bs=p_bs, stats=stats, stats_bs=stats_bs, d_bs=d_bs, d2_bs=d2_bs,
+                                         ldd=ldd, lnb=lnb))
     d = _lib.GemmDesc()
     d.m, d.n, d.k, d.batch = m, n, k, batch
     d.math = _lib.JG_MATH_TF32X3 if fp32 else _lib.JG_MATH_BF16
@@ -157,6 +173,55 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
         GEMM_TIMER.append((s, e, 2 * m * n * k * batch, nbytes))
     else:
         _lib.gemm_raw(d)
+    return out
+
+
+def _at(t: torch.Tensor | None, off: int):
+    """Flat view of `t` starting `off` elements in (a batch item of a strided operand)."""
+    return None if t is None else t.reshape(-1)[off:]
+
+
+def _gemm_tf32x3_chunked(out, a, a_lo, b, b_lo, m, n, k, batch, a_bs, b_bs, lda, ldb, reduce_batch, ep):
+    """fp32-mode GEMM with K accumulated in TF32X3_KCHUNK-long chunks: one batched jg_gemm per
+    output item writes the chunk products as fp32 planes, jg_epilogue sums the planes in order
+    and applies the epilogue (bias / residual / GELU / moments / accumulate); the layer-norm
+    backward moments (JG_EPI_LNB) follow from jg_ln_bwd_moments on the finished output."""
+    kc = TF32X3_KCHUNK
+    S, tail = k // kc, k % kc
+    per = S + (1 if tail else 0)
+    epi = ep["epi"]
+    lnb = ep["lnb"]
+    ldd = ep["ldd"] if ep["ldd"] is not None else n
+    d_bs = ep["d_bs"] if ep["d_bs"] is not None else (0 if reduce_batch else m * n)
+    d2_bs = ep["d2_bs"] if ep["d2_bs"] is not None else (0 if reduce_batch else m * n)
+    r_bs = ep["r_bs"] if ep["r_bs"] else m * n
+    p_bs = ep["p_bs"] if ep["p_bs"] else m * n
+    st_bs = ep["stats_bs"] if ep["stats_bs"] else 2 * m
+    outs = [None] if reduce_batch else list(range(batch))
+    for o in outs:
+        items = list(range(batch)) if reduce_batch else [o]
+        planes = torch.empty((len(items) * per, m, n), dtype=torch.float32, device=a.device)
+        for j, bi in enumerate(items):
+            pl = planes[j * per:]
+            gemm_into(pl, _at(a, bi * a_bs), _at(b, bi * b_bs), _lib.JG_KMAJOR, _lib.JG_KMAJOR, m, n, kc, S, kc, kc,
+                      a_lo=_at(a_lo, bi * a_bs), b_lo=_at(b_lo, bi * b_bs), lda=lda, ldb=ldb, d_bs=m * n)
+            if tail:
+                off = S * kc
+                gemm_into(pl[S], _at(a, bi * a_bs + off), _at(b, bi * b_bs + off), _lib.JG_KMAJOR, _lib.JG_KMAJOR,
+                          m, n, tail, a_lo=_at(a_lo, bi * a_bs + off), b_lo=_at(b_lo, bi * b_bs + off), lda=lda, ldb=ldb)
+        ob = 0 if o is None else o
+        from . import kernels as K
+        K.epilogue(planes, m, n, nplanes=planes.shape[0], acc_bs=m * n, epi=epi & ~_lib.EPI_LNB, alpha=ep["alpha"],
+                   d=_at(out, ob * d_bs), ldd=ldd, d2=_at(ep["d2"], ob * d2_bs), ldd2=n,
+                   bias=_at(ep["bias"], ob * ep["bias_bs"]), resid=_at(ep["resid"], ob * r_bs),
+                   pre=_at(ep["pre"], ob * p_bs), stats=_at(ep["stats"], ob * st_bs))
+        if epi & _lib.EPI_LNB:
+            lx, lg, lmr = lnb[:3]
+            ldx = lnb[3] if len(lnb) > 3 else n
+            if ldx != n or ldd != n:
+                raise ShapeError("chunked 3xTF32 GEMM: JG_EPI_LNB needs contiguous rows")
+            K.ln_bwd_moments(_at(lx, ob * m * ldx), _at(out, ob * d_bs), lg, _at(lmr, ob * st_bs),
+                             _at(ep["stats"], ob * st_bs), m, n)
     return out
 
 

@@ -235,6 +235,27 @@ def _unpatchify(tok, batch, lat, lon, chans, pl, pw):
     return t.reshape(batch, lat, lon, chans)
 
 
+def gelu_fwd(x, y):
+    y.copy_(_gelu(x.double()).to(y.dtype))
+
+
+def gelu_bwd(x, g, dx):
+    dx.copy_((g.double() * _gelu_grad(x.double())).to(dx.dtype))
+
+
+def matmul(a, b, mode="NN"):
+    """tensor.matmul on CPU: exact float64 product, cast to the operand dtype."""
+    from paper_2507_05753_b200.tensor import MatmulMode, _check_operands
+    _check_operands(a, b, mode)
+    mode = MatmulMode(mode)
+    A, B = a.double(), b.double()
+    if mode is MatmulMode.NT:
+        B = B.transpose(-1, -2)
+    elif mode is MatmulMode.TN:
+        A = A.transpose(-1, -2)
+    return torch.matmul(A, B).to(a.dtype)
+
+
 def ln_moments(x, stats, rows, cols):
     xv = x.reshape(rows, cols).double()
     stats.view(rows, 2)[:, 0] += xv.sum(1).float()
@@ -372,7 +393,7 @@ def step_increment(counter):
 
 NAMES = ["gemm", "epilogue", "sum_planes", "axpy", "cast_bf16", "patchify", "ln_moments", "ln_apply", "ln_bwd_moments",
          "ln_bwd_apply", "colsum", "rowsum", "blend_loss", "adam", "step_increment", "sqnorm", "opt_schedule",
-         "copy_async"]
+         "copy_async", "gelu_fwd", "gelu_bwd"]
 
 
 def install():
@@ -381,3 +402,5 @@ def install():
     mod = globals()
     for name in NAMES:
         setattr(K, name, mod[name])
+    import paper_2507_05753_b200.tensor as T
+    T.matmul = matmul

@@ -157,3 +157,62 @@ def test_lnb_epilogue_moments(cuda, batch, m, n, k):
     xhat = (x.double().reshape(batch * m, n) - mr[:, :1].double()) * mr[:, 1:].double()
     want = torch.stack([h.sum(1), (h * xhat).sum(1)], 1)
     assert rel_err(stats.double().cpu().numpy(), want.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("majors", [(0, 0), (1, 1), (0, 1)])
+@pytest.mark.parametrize("k", [4320, 16380])
+def test_tf32x3_long_k_accuracy(cuda, majors, k):
+    """fp32 mode at the C4 contraction lengths: tcgen05's fp32 accumulation truncates, so long-K
+    3xTF32 GEMMs accumulate K-chunks into planes summed round-to-nearest (tensor.TF32X3_KCHUNK);
+    without the chunking K = 16380 measured 2.2e-4 (tools/f32_diag.py)."""
+    from paper_2507_05753_b200 import _lib, tensor as T
+    am, bm = majors
+    gen = torch.Generator(device="cuda").manual_seed(k + 10 * am + bm)
+    m, n = 384, 272
+    a = torch.randn((m, k) if am == 0 else (k, m), device=cuda, generator=gen)
+    b = torch.randn((n, k) if bm == 0 else (k, n), device=cuda, generator=gen)
+    bias = torch.randn(n, device=cuda, generator=gen)
+    out = torch.empty(m, n, device=cuda)
+    d2 = torch.empty(m, n, device=cuda)
+    st = torch.zeros(m, 2, device=cuda)
+    T.gemm_into(out, a, b, am, bm, m, n, k, epi=_lib.EPI_BIAS_COL | _lib.EPI_GELU_FWD | _lib.EPI_STATS,
+                bias=bias, d2=d2, stats=st)
+    torch.cuda.synchronize()
+    ref = (a.double() if am == 0 else a.double().t()) @ (b.double().t() if bm == 0 else b.double()) + bias.double()
+    e = rel_err(out.cpu().numpy(), ref.cpu().numpy())
+    print(f"3xTF32 majors {am}{bm} K={k}: rel {e:.2e}")
+    assert e < 2e-5, e
+    gref = ref * 0.5 * (1 + torch.erf(ref / np.sqrt(2)))
+    assert rel_err(d2.cpu().numpy(), gref.cpu().numpy()) < 2e-5
+    assert rel_err(st[:, 1].cpu().numpy(), (ref * ref).sum(1).cpu().numpy()) < 2e-5
+
+
+def test_tf32x3_long_k_lnb_and_reduce_batch(cuda):
+    """Chunked 3xTF32 with the layer-norm-backward moments (JG_EPI_LNB -> jg_ln_bwd_moments on the
+    finished output) and with a batch folded into K (reduce_batch, weight gradients)."""
+    from paper_2507_05753_b200 import _lib, tensor as T
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    m, n, k = 256, 320, 8640
+    a = torch.randn(m, k, device=cuda, generator=gen)
+    b = torch.randn(n, k, device=cuda, generator=gen)
+    x = torch.randn(m, n, device=cuda, generator=gen)
+    gamma = torch.randn(n, device=cuda, generator=gen)
+    mr = torch.stack([torch.randn(m, device=cuda, generator=gen), torch.rand(m, device=cuda, generator=gen) + 0.5], 1)
+    out = torch.empty(m, n, device=cuda)
+    stats = torch.zeros(m, 2, device=cuda)
+    T.gemm_into(out, a, b, _lib.JG_KMAJOR, _lib.JG_KMAJOR, m, n, k, epi=_lib.EPI_LNB, stats=stats, lnb=(x, gamma, mr))
+    ref = a.double() @ b.double().t()
+    assert rel_err(out.cpu().numpy(), ref.cpu().numpy()) < 2e-5
+    h = ref * gamma.double()[None, :]
+    xhat = (x.double() - mr[:, :1].double()) * mr[:, 1:].double()
+    want = torch.stack([h.sum(1), (h * xhat).sum(1)], 1)
+    assert rel_err(stats.cpu().numpy(), want.cpu().numpy()) < 2e-5
+    # reduce_batch: dW[t, j] = sum_b sum_e u[b, t, e] gh[b, e, j], K = e long
+    bsz, t, e, dt = 2, 192, 4480, 160
+    u = torch.randn(bsz, t, e, device=cuda, generator=gen)
+    gh = torch.randn(bsz, e, dt, device=cuda, generator=gen)
+    dw = torch.zeros(t, dt, device=cuda)
+    T.gemm_into(dw, u, gh, _lib.JG_KMAJOR, _lib.JG_MNMAJOR, t, dt, e, bsz, t * e, e * dt, reduce_batch=True,
+                epi=_lib.EPI_ACCUM)
+    want = torch.einsum("bte,bej->tj", u.double(), gh.double())
+    assert rel_err(dw.cpu().numpy(), want.cpu().numpy()) < 2e-5

@@ -14,8 +14,7 @@ from paper_2507_05753_b200.engine import TrainStep
 comm = Communicator.from_env()
 ctx = MpContext(comm, list(range(comm.world_size)))
 cfg_kw, lat_real, vars_real, _ = bench.CONFIGS[os.environ.get("CFG", "C4")]
-model = WeatherMixerModel(ctx, ModelConfig(**cfg_kw), init="fast")
-model.lat_real, model.vars_real = lat_real, vars_real
+model = WeatherMixerModel(ctx, ModelConfig(**cfg_kw), init="fast", lat_real=lat_real, vars_real=vars_real)
 step = TrainStep(model)
 xd, td = bench.fill_random_inputs(step, lat_real, 1234 + ctx.pos)
 for _ in range(3):

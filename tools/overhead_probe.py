@@ -16,8 +16,7 @@ from paper_2507_05753_b200.engine import TrainStep
 comm = Communicator.from_env()
 ctx = MpContext(comm, list(range(comm.world_size)))
 cfg_kw, lat_real, vars_real, _ = bench.CONFIGS[os.environ.get("CFG", "C4")]
-model = WeatherMixerModel(ctx, ModelConfig(**cfg_kw), init="fast")
-model.lat_real, model.vars_real = lat_real, vars_real
+model = WeatherMixerModel(ctx, ModelConfig(**cfg_kw), init="fast", lat_real=lat_real, vars_real=vars_real)
 noop = lambda *a, **k: None  # noqa: E731
 orig = {"barrier": TR.SymmTransport.barrier, "ar_row": MpContext.all_reduce_row, "ar_col": MpContext.all_reduce_col,
         "copy": K.copy_async, "epilogue": K.epilogue}
