@@ -221,6 +221,32 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
+
+
+def comm_roofline(model, batch, ms, gemm_peak_tflops):
+    """Jigsaw communication roofline of one rank (None at n = 1): the bytes this schedule sends
+    over NVLink per step (jigsaw_grid.step_exchange_bytes, checked against the transports' own
+    counters in tests/test_jigsaw_cpu.py), their minimum time at the measured 770 GB/s per
+    direction, the rank's GEMM FLOPs at the sustained bf16 peak, and the fused compute+collective
+    roofline target = the slower of the two, against the measured step."""
+    if model.ctx.n == 1:
+        return None
+    from paper_2507_05753_b200.jigsaw_grid import step_exchange_bytes
+    v = step_exchange_bytes(model, batch, 1)
+    fl = sum(model.step_flops(batch, 1))
+    t_comm = v["total"] / (NVLINK_GBS * 1e9) * 1e3
+    t_gemm = fl / (gemm_peak_tflops * 1e12) * 1e3
+    target = max(t_comm, t_gemm)
+    return {"grid": f"{model.R}x{model.C}", "nvlink_bytes_per_step_per_rank": v["total"],
+            "exchange_bytes": v["exchange"], "allreduce_bytes": v["allreduce"],
+            "avg_gbs_over_step": v["total"] / (ms / 1e3) / 1e9, "peak_gbs": NVLINK_GBS,
+            "t_comm_min_ms": t_comm, "t_gemm_min_ms": t_gemm, "roofline_step_ms": target,
+            "frac": target / ms, "bound": "nvlink" if t_comm > t_gemm else "tensor",
+            "basis": "per-rank bytes of the balanced schedule / measured 770 GB/s peer copy; rank GEMM FLOPs / "
+                     "sustained bf16 peak; frac = roofline step / measured step"}
+
+
 def fill_random_inputs(step, lat_real, seed):
     """Synthetic z-scored inputs in the step's resident buffers: x, target ~ N(0, 1), padded rows
     zero (random data matters: the GEMMs are power-capped and zero operands draw less power)."""
@@ -377,6 +403,7 @@ def run_ours(args, rank, world):
                     "api": "TrainStep.__call__(x_host_pinned, target_host_pinned, prefetch_next=(x, target)) -> float loss",
                     "input_pipelining": ("each step's H2D copy of the next step's inputs overlaps its compute" if prefetch
                                          else "none: each step copies its own inputs")},
+            "comm": comm_roofline(model, args.batch, ms, sustained),
             "gpu_launches": (step.launches_per_step or 0) * args.steps,
             "launches_per_step": step.launches_per_step,
             "fused_adam": step.fused_adam,

@@ -228,6 +228,7 @@ class TrainStep:
             self._body_bwd()
             self.launches_per_step = _lib.launch_count() - before
         self._updated()
+        self.model.ctx.flops += sum(self.model.step_flops(self.batch, self.r))  # MpContext counter, per step
         return self.ws.loss
 
     def _streams(self):

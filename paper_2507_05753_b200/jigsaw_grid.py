@@ -89,19 +89,27 @@ class GridWorkspace:
         else:
             self.row = NcclTransport(ctx.row_group, C, m.c, dev) if C > 1 else None
             self.col = NcclTransport(ctx.col_group, R, m.r, dev) if R > 1 else None
-            for tr, spec in ((self.row, row_persist), (self.col, col_persist)):
-                if tr is not None:
-                    for name, shape, dt in spec:
-                        tr.reserve(name, shape, dt)
+        if C == 1:
+            # R x 1 grids (JIGSAW_GRID, e.g. 2x1 / 4x1): the row group is this rank alone — a
+            # one-member transport whose gathers / reduce-scatters are local copies
+            self.row = NcclTransport(None, 1, 0, dev)
+        for tr, spec in ((self.row, row_persist), (self.col, col_persist)):
+            if tr is not None and tr.kind == "nccl":
+                for name, shape, dt in spec:
+                    tr.reserve(name, shape, dt)
         self.kind = kind
-        # GEMM + reduce-scatter + epilogue in one kernel (symmetric-memory transport)
-        self.fused = kind == "symm" and fused_rs_enabled()
+        # GEMM + reduce-scatter + epilogue in one kernel (symmetric-memory transport, both axes)
+        self.fused = kind == "symm" and fused_rs_enabled() and C > 1
         # reduce-scatter partial planes travel in the operand dtype (bf16 mode: half the NVLink bytes
         # and half the epilogue reads; summed in fp32); JIGSAW_PARTIALS=fp32 keeps fp32 partials
         bf = od == torch.bfloat16 and os.environ.get("JIGSAW_PARTIALS", "bf16") != "fp32"
         self.pdt = torch.bfloat16 if bf else F32
         self.dgrad = torch.empty(max(kin_max, E * Kl), dtype=F32, device=dev)  # reduced weight gradients
         self.panels = {n: self.col.persistent(f"panel:{n}").view(panel_shape[_base(n)]) for n in self.panel_names}
+        # live buffers of received parameter blocks (reference MpContext.param_buffer_peak,
+        # parallel.py:71-76): the peers' planes of every gathered weight panel, held for the step
+        held = sum(p.numel() * (R - 1) // R for p in self.panels.values())
+        ctx.param_buffer_peak = max(ctx.param_buffer_peak, held)
 
 
 def _gw(m, ws) -> GridWorkspace:
@@ -140,6 +148,7 @@ def panel_push_segments(m, g, lo: int, hi: int):
         nbytes = op.numel() * es
         off = g.col._slot_off(f"panel:{name}", 0, nbytes) + g.col.idx * nbytes
         segs.append((start - lo, op.numel(), [g.col.base[j] + off for j in range(g.col.G)]))
+        g.col.bytes_sent += (g.col.G - 1) * nbytes  # the optimiser's stores into the peers' panel slots
     return segs
 
 
@@ -419,3 +428,63 @@ def grad_sync(m) -> None:
         lo, hi = f.kind_range[(cls, "vec_row")]
         if hi > lo and m.C > 1:
             ctx.all_reduce_row(f.grad[lo:hi])
+
+
+# --------------------------------------------------------------------------- comm roofline
+def step_exchange_bytes(m, batch: int, r: int = 1, op_bytes: int | None = None, part_bytes: int | None = None) -> dict:
+    """Bytes ONE rank sends to its peers over NVLink in one training step of this schedule
+    (forward_grid, the loss's decoder-gradient push, backward_grid, grad_sync, the weight-panel
+    gathers / Adam pushes) — the balanced-grid counterpart of the reference's analytic tables
+    (parallel.py:361-466, model.py:483-529), in bytes rather than elements because the operands
+    (bf16) and partials (bf16 or fp32) have different widths. Every rank of the grid sends the
+    same amount. Returns {"exchange": gathers + reduce-scatters (transport payload),
+    "allreduce": the small NCCL all-reduces (ring: 2 (G-1)/G of the buffer), "total"}.
+    Checked against the transports' own byte counters in tests/test_jigsaw_cpu.py."""
+    cfg = m.cfg
+    R, C = m.R, m.C
+    if m.ctx.n == 1:
+        return {"exchange": 0, "allreduce": 0, "total": 0}
+    sop = op_bytes if op_bytes is not None else torch.empty((), dtype=m.op_dtype).element_size()
+    if part_bytes is None:
+        bf = m.op_dtype == torch.bfloat16 and os.environ.get("JIGSAW_PARTIALS", "bf16") != "fp32"
+        part_bytes = 2 if bf else 4
+    sp = part_bytes
+    E, H, F, Kd, T = cfg.d_emb, cfg.d_ch, cfg.patch_features, cfg.d_tok, cfg.tokens
+    Tl, El, Er, Kl, Hl, Fl = T // R, E // C, E // R, Kd // C, H // C, F // C
+    B, nj = batch, r * cfg.n_blocks
+    M = B * Tl
+    ex = 0
+    # weight panels of the channel layers, gathered (or Adam-pushed) over the column group
+    if R > 1:
+        ex += (R - 1) * (E * Fl + F * El + cfg.n_blocks * (H * El + E * Hl)) // R * sop
+    rs_row = lambda cols: (C - 1) * M * cols * sp  # noqa: E731  channel-layer / token RS over the row group
+    push_row = lambda cols: (C - 1) * M * cols * sop  # noqa: E731
+    # forward: enc, dec, and per pass ch1 / ch2 reduce-scatters; LN1 output pushes; token layers
+    ex += rs_row(E // C) + rs_row(F // C)
+    ex += nj * (rs_row(H // C) + rs_row(E // C) + push_row(El))
+    ex += nj * B * ((R - 1) * Er * Kl * (sp + sop) + (C - 1) * Tl * El * sp)
+    # loss: the decoder-output gradient pushed to the row group
+    ex += push_row(Fl)
+    # backward: dec dX copy push, per block gc / g_x2 / g pushes, token RS + gh push, dW RS (column)
+    ex += push_row(El)
+    ex += nj * (push_row(Hl) + push_row(El) + push_row(El))
+    ex += nj * B * ((R - 1) * Er * Kl * (sp + sop) + (C - 1) * Tl * El * sp)
+    if R > 1:
+        dw = F * El + nj * (E * Hl + H * El) + E * Fl  # dec, per pass ch2 / ch1, enc weight-gradient planes
+        ex += (R - 1) * dw // R * sp
+    # small all-reduces: LN moments (fwd 2 per pass, bwd 2 per pass, [M, 2] fp32) over the row
+    # group, the loss over the grid, duplicated-vector gradients over their sharing groups
+    ar = 0.0
+    ring = lambda G, nbytes: 2.0 * (G - 1) / G * nbytes  # noqa: E731
+    if C > 1:
+        ar += 4 * nj * ring(C, M * 2 * 4)
+    ar += ring(m.ctx.n, 4)
+    f = m.flat
+    for cls in f.CLASSES:
+        lo, hi = f.kind_range[(cls, "vec_col")]
+        if hi > lo and R > 1:
+            ar += ring(R, (hi - lo) * 4)
+        lo, hi = f.kind_range[(cls, "vec_row")]
+        if hi > lo and C > 1:
+            ar += ring(C, (hi - lo) * 4)
+    return {"exchange": int(ex), "allreduce": int(ar), "total": int(ex + ar)}

@@ -329,6 +329,17 @@ class WeatherMixerModel:
         li = self.layouts[name].to_local_index(self.ctx.pos, idx)
         return None if li is None else float(self.params[name].data[li])
 
+    def step_flops(self, batch: int, r: int = 1) -> tuple[int, int]:
+        """(forward, backward) GEMM FLOPs THIS rank executes per call, counted like the reference's
+        MpContext._mm (2 * out.size * k per GEMM, parallel.py:65-69). Every rank of the balanced
+        grid does exactly 1/n of them. The backward skips the encoder's input gradient, which the
+        reference computes and discards (model.py:444-445): 2 T F E per sample fewer."""
+        cfg, n = self.cfg, self.ctx.n
+        T, F, E = cfg.tokens, cfg.patch_features, cfg.d_emb
+        fwd = batch * (4 * T * F * E + r * cfg.n_blocks * 4 * T * E * (cfg.d_tok + cfg.d_ch))
+        bwd = 2 * fwd - batch * 2 * T * F * E
+        return fwd // n, bwd // n
+
     def step_comm_volume(self, batch: int, r: int = 1) -> int:
         """Elements the REFERENCE schedules send per fwd+bwd (model.py:483-529), for n = 1, 2, 4."""
         cfg, n = self.cfg, self.ctx.n
@@ -376,6 +387,7 @@ class WeatherMixerModel:
         out = torch.empty_like(ws.xin)
         self._blend(ws, out=out)
         self._cache_valid = True
+        self.ctx.flops += self.step_flops(ws.B, r)[0]
         return out
 
     def backward(self, g_out: torch.Tensor) -> None:
@@ -387,6 +399,7 @@ class WeatherMixerModel:
         g_out = self._check_sample(g_out)
         self._blend(ws, g_ext=g_out)
         self._backward(ws)
+        self.ctx.flops += self.step_flops(ws.B, ws.r)[1]
 
     def grad_sync(self) -> None:
         """Sum gradients of duplicated vector parameters over their sharing group (model.py:451-460)."""

@@ -51,6 +51,7 @@ class MpContext:
         self.R, self.C = grid_shape(self.n)
         self.r, self.c = self.pos // self.C, self.pos % self.C
         self.flops = 0
+        self.allreduce_bytes = 0.0  # ring all-reduce payload this rank sends (2 (G-1)/G per buffer)
         self.param_buffer_elements = 0
         self.param_buffer_peak = 0
         self.row_ranks = [group[self.r * self.C + j] for j in range(self.C)]
@@ -160,8 +161,12 @@ class MpContext:
         dist.reduce_scatter_tensor(out.view(-1), planes.reshape(-1), group=self.col_group)
         return out
 
+    def _ar_count(self, G: int, x: torch.Tensor) -> None:
+        self.allreduce_bytes += 2.0 * (G - 1) / G * x.numel() * x.element_size()
+
     def all_reduce_all(self, x: torch.Tensor) -> torch.Tensor:
         if self.n > 1:
+            self._ar_count(self.n, x)
             dist.all_reduce(x, group=self.mp_group)
         return x
 
@@ -175,11 +180,13 @@ class MpContext:
 
     def all_reduce_row(self, x: torch.Tensor) -> torch.Tensor:
         if self.C > 1:
+            self._ar_count(self.C, x)
             dist.all_reduce(x, group=self.row_group)
         return x
 
     def all_reduce_col(self, x: torch.Tensor) -> torch.Tensor:
         if self.R > 1:
+            self._ar_count(self.R, x)
             dist.all_reduce(x, group=self.col_group)
         return x
 

@@ -49,6 +49,7 @@ class NcclTransport:
         self.group, self.G, self.idx, self.device = group, G, idx, device
         self._persist: dict[str, torch.Tensor] = {}
         self._scratch = {}
+        self.bytes_sent = 0  # payload bytes this member sends to its peers (host-side count per issue)
 
     def reserve(self, name: str, shape, dtype) -> None:
         self._persist[name] = torch.empty(shape, dtype=dtype, device=self.device)
@@ -74,6 +75,7 @@ class NcclTransport:
     def ag(self, x: torch.Tensor, slot: str = "tmp", sub: int = 0, nsub: int = 1) -> torch.Tensor:
         """Planes [G, *x.shape] in the named slot (viewed [nsub, G, *x.shape], entry sub)."""
         out = self._slot(slot, nsub * self.G * x.numel(), x.dtype).view(nsub, self.G, *x.shape)[sub]
+        self.bytes_sent += (self.G - 1) * x.numel() * x.element_size()
         if self.G == 1:
             out[0].copy_(x)
         else:
@@ -88,6 +90,7 @@ class NcclTransport:
         return Gather(planes, self._buf(("own", slot), n, dtype).view(*shape), [])
 
     def publish(self, h: Gather) -> None:
+        self.bytes_sent += (self.G - 1) * h.own.numel() * h.own.element_size()
         if self.G == 1:
             h.planes[0].copy_(h.own)
         else:
@@ -98,6 +101,7 @@ class NcclTransport:
         planes = self._buf("rs", self.G * rows * cols, dtype).view(self.G, rows, cols)
         for s in range(q):
             fn(s, planes[s], q * rows * cols, None)
+        self.bytes_sent += (self.G - 1) * rows * cols * planes.element_size()
         if self.G == 1:
             return planes[0], 1, 0
         use_out = out is not None and out.dtype == dtype
@@ -133,6 +137,7 @@ class SymmTransport:
         self.flag_off = off + 2 * self.scratch_bytes  # per region: FLAG_CAP arrival counters (fused RS)
         self.bar_off = self.flag_off + 2 * FLAG_CAP * 4  # G arrival counters of jg_group_barrier
         self.k = 0
+        self.bytes_sent = 0  # payload bytes this member stores into its peers (host-side count per issue)
         self._alloc(self.bar_off + 256)
         self.buf[self.flag_off:].zero_()
         # JIGSAW_BARRIER=jg: jg_group_barrier (one 32-thread kernel: release-add into each peer's
@@ -195,6 +200,7 @@ class SymmTransport:
         x = x.contiguous()
         for j in range(self.G):  # push my block into slot idx of every member (copy engine)
             K.copy_async(self.base[j] + off + self.idx * nbytes, x, nbytes)
+        self.bytes_sent += (self.G - 1) * nbytes
         self.barrier()
         return self._view(off, (self.G, *x.shape), x.dtype)
 
@@ -209,6 +215,7 @@ class SymmTransport:
         return Gather(planes, planes[self.idx], peers)
 
     def publish(self, h: Gather) -> None:
+        self.bytes_sent += len(h.peers) * h.own.numel() * h.own.element_size()
         self.barrier()
 
     def rs_gemm(self, rows: int, cols: int, dtype, fn, q: int = 1, out: torch.Tensor | None = None):
@@ -220,6 +227,7 @@ class SymmTransport:
         # owner plane o of my partial goes to slot idx of member o's region (remote epilogue stores)
         for s in range(q):
             fn(s, local[0], 0, [self.base[j * q + s] + off + self.idx * pbytes for j in range(self.G // q)])
+        self.bytes_sent += (self.G - 1) * pbytes
         self.barrier()
         return local, self.G, rows * cols
 
@@ -243,6 +251,7 @@ class SymmTransport:
             assert bad not in epi, f"fused reduce-scatter epilogue: unsupported argument {bad}"
         part = _lib.dtype_code(local)
         nb = self.G // q
+        self.bytes_sent += (self.G - 1) * pbytes
         for s in range(q):
             dpl, fpeers, own = [], [], -1
             for j in range(nb):

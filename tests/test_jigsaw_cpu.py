@@ -39,6 +39,8 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
         import cpu_kernels
         cpu_kernels.install()
         opts = opts or {}
+        if "grid" in opts:
+            os.environ["JIGSAW_GRID"] = opts["grid"]
         if "fused_rs" in opts:
             os.environ["JIGSAW_FUSED_RS"] = opts["fused_rs"]
         if opts.get("transport") == "shm":
@@ -120,6 +122,30 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
                 dist.barrier()
                 dist.destroy_process_group()
             return
+        if mode == "comm":
+            # one step warms the panels, the second is the steady state: its transport / all-reduce
+            # byte counters must equal the analytic per-step volume of the schedule
+            from paper_2507_05753_b200.engine import TrainStep
+            from paper_2507_05753_b200.jigsaw_grid import step_exchange_bytes
+            tl = om.local_sample(oc, z["g_out"][:1] * 0.5, ctx.R, ctx.C, ctx.r, ctx.c)
+            step = TrainStep(model, batch=1, graph=False)
+            step.ws.xin.copy_(torch.tensor(xl[:1], dtype=torch.float32))
+            step.target.copy_(torch.tensor(tl, dtype=torch.float32))
+
+            def counters():
+                gw = step.ws.grid
+                return sum(t.bytes_sent for t in (gw.row, gw.col) if t is not None), ctx.allreduce_bytes
+            step.run_device()
+            c1 = counters()
+            step.run_device()
+            c2 = counters()
+            out_q.put({"pos": ctx.pos, "rank": rank, "measured": (c2[0] - c1[0], c2[1] - c1[1]),
+                       "analytic": step_exchange_bytes(model, 1, 1)})
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+                dist.destroy_process_group()
+            return
         if mode == "pushcmp":
             from paper_2507_05753_b200.engine import TrainStep
             tl = om.local_sample(oc, z["g_out"][:1] * 0.5, ctx.R, ctx.C, ctx.r, ctx.c)
@@ -166,9 +192,10 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
         model.grad_sync()
         if opts.get("transport") == "shm":
             g = model._ws.grid
-            assert type(g.row if g.row is not None else g.col).__name__ == "ShmSymmTransport"
+            assert type(g.row if g.row is not None and g.row.G > 1 else g.col).__name__ == "ShmSymmTransport"
         res = {"pos": ctx.pos, "out": out.numpy(), "grads": {k: p.grad.numpy().copy() for k, p in model.params.items()},
-               "rc": (ctx.R, ctx.C, ctx.r, ctx.c)}
+               "rc": (ctx.R, ctx.C, ctx.r, ctx.c), "flops": ctx.flops, "buf_peak": ctx.param_buffer_peak,
+               "batch": int(xl.shape[0])}
         out_q.put(res)
         if world > 1:
             import torch.distributed as dist
@@ -203,6 +230,15 @@ def _check(world, r=1, opts=None):
     out_key = "out_f64" if r == 1 else "rollout_out_f64"
     gpre = "grad_f64/" if r == 1 else "rollout_grad_f64/"
     ref_out = z[out_key]
+    if r == 1:
+        # MpContext.flops on the fused path: the reference's count (golden, parallel.py:65-69) minus
+        # the encoder input gradient it computes and discards, split evenly over the ranks
+        B = res[0]["batch"]
+        want = meta["flops_n1"] - 2 * B * oc.tokens * oc.patch_features * oc.d_emb
+        assert sum(d["flops"] for d in res) == want
+        assert len({d["flops"] for d in res}) == 1
+        R = res[0]["rc"][0]
+        assert all((d["buf_peak"] > 0) == (R > 1) for d in res)
     for d in res:
         R, C, rr, cc = d["rc"]
         assert rel_err(d["out"], om.local_sample(oc, ref_out, R, C, rr, cc)) < 1e-5
@@ -458,3 +494,29 @@ def test_adam_panel_push_matches_gathers(world):
         assert a["losses"] == b["losses"], (a["losses"], b["losses"])
         for k in a["params"]:
             assert np.array_equal(a["params"][k], b["params"][k]), k
+
+
+@pytest.mark.parametrize("world,grid,transport", [(2, "2x1", "nccl"), (2, "2x1", "shm"), (4, "4x1", "nccl"),
+                                                   (4, "4x1", "shm"), (8, "8x1", "shm")])
+def test_grid_override_matches_reference(world, grid, transport):
+    """JIGSAW_GRID: the R > C owner-sub-chunk path (q = R / C = 2, 4: the 4 x 2 grid's) and other
+    factorisations on the real schedule, both transports, against the reference's n = 1 golden."""
+    _check(world, opts={"grid": grid, "transport": transport})
+
+
+@pytest.mark.parametrize("world,transport,dtype,grid", [(2, "nccl", "f32", None), (4, "shm", "bf16", None),
+                                                        (8, "shm", "bf16", None), (8, "nccl", "f32", None),
+                                                        (4, "shm", "bf16", "4x1")])
+def test_comm_volume_matches_analytic(world, transport, dtype, grid):
+    """Comm roofline numerator: the bytes each rank's transports and all-reduces actually issue in
+    a steady-state training step equal jigsaw_grid.step_exchange_bytes (the schedule's analytic
+    volume, the balanced-grid counterpart of the reference's comm_volume tables)."""
+    opts = {"transport": transport, "dtype": dtype}
+    if grid:
+        opts["grid"] = grid
+    res = _run(world, mode="comm", opts=opts)
+    for d in res:
+        ex, ar = d["measured"]
+        assert ex == d["analytic"]["exchange"], (d["pos"], ex, d["analytic"])
+        assert abs(ar - d["analytic"]["allreduce"]) <= 1e-6 * max(1.0, ar), (d["pos"], ar, d["analytic"])
+        assert ex > 0

@@ -29,6 +29,27 @@ def test_jigsaw_nccl_parity(n):
         assert res[key]["out"] < tol and res[key]["grad"] < tol, (key, res[key])
 
 
+@pytest.mark.parametrize("n,grid", [(2, "2x1"), (4, "4x1")])
+def test_jigsaw_grid_override_parity(n, grid):
+    """R x 1 grids (JIGSAW_GRID): the R > C column-group owner-sub-chunk path (q = R / C = 2, 4 —
+    the 4 x 2 grid's q = 2 reduce-scatters) over real NVLink on 2 / 4 GPUs: golden parity, and
+    the peer-memory transport bit-identical to NCCL."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    env = dict(os.environ, JIGSAW_GRID=grid, MPCHECK_TRANSPORTS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29569", os.path.join(HERE, "mp_check.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    line = [ln for ln in p.stdout.splitlines() if ln.startswith("MPCHECK ")]
+    assert p.returncode == 0 and line, p.stdout[-3000:] + p.stderr[-3000:]
+    res = json.loads(line[0][len("MPCHECK "):])
+    print(res)
+    assert res["grid"] == [int(v) for v in grid.split("x")]
+    for key, tol in (("G1_f32", 1e-4), ("C2_f32", 1e-4), ("G1_bf16", 2e-2), ("C2_bf16", 2e-2)):
+        assert res[key]["out"] < tol and res[key]["grad"] < tol, (key, res[key])
+    assert res["symm_vs_nccl_f32"] == 0.0 and res["symm_vs_nccl_bf16"] == 0.0, res
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_symmetric_memory_transport_matches_nccl(n):
     """Peer-memory gathers and GEMM-epilogue reduce-scatters equal NCCL's, bit for bit."""
