@@ -33,7 +33,7 @@ def test_jigsaw_nccl_parity(n):
 def test_jigsaw_grid_override_parity(n, grid):
     """R x 1 grids (JIGSAW_GRID): the R > C column-group owner-sub-chunk path (q = R / C = 2, 4 —
     the 4 x 2 grid's q = 2 reduce-scatters) over real NVLink on 2 / 4 GPUs: golden parity, and
-    the peer-memory transport bit-identical to NCCL."""
+    the peer-memory transport against NCCL on the same step."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     env = dict(os.environ, JIGSAW_GRID=grid, MPCHECK_TRANSPORTS="1")
@@ -47,17 +47,22 @@ def test_jigsaw_grid_override_parity(n, grid):
     assert res["grid"] == [int(v) for v in grid.split("x")]
     for key, tol in (("G1_f32", 1e-4), ("C2_f32", 1e-4), ("G1_bf16", 2e-2), ("C2_bf16", 2e-2)):
         assert res[key]["out"] < tol and res[key]["grad"] < tol, (key, res[key])
-    assert res["symm_vs_nccl_f32"] == 0.0 and res["symm_vs_nccl_bf16"] == 0.0, res
+    # (not bitwise: the layer-norm row moments are accumulated with atomics across tiles, so two
+    # runs differ in the last bits whatever the transport; bit-exactness of the transports
+    # themselves, q-sub-chunked reduce-scatters included, is transport_check.py's)
+    assert res["symm_vs_nccl_f32"] < 1e-4 and res["symm_vs_nccl_bf16"] < 2e-2, res
 
 
-@pytest.mark.parametrize("n", [2, 4])
-def test_symmetric_memory_transport_matches_nccl(n):
-    """Peer-memory gathers and GEMM-epilogue reduce-scatters equal NCCL's, bit for bit."""
+@pytest.mark.parametrize("n,grid", [(2, None), (4, None), (2, "2x1"), (4, "4x1")])
+def test_symmetric_memory_transport_matches_nccl(n, grid):
+    """Peer-memory gathers and GEMM-epilogue reduce-scatters (q-sub-chunked ones included) equal
+    NCCL's, bit for bit."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", "--master-port=29563", os.path.join(HERE, "transport_check.py")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    env = dict(os.environ, JIGSAW_GRID=grid) if grid else None
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert "TRANSPORT_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
 
 

@@ -38,7 +38,22 @@ for axis in ("row", "col"):
     sa, sn, sp = st.rs_gemm(64, 48, torch.float32, fn)
     ssum = sum(sa.reshape(-1)[i * sp:(i + 1) * sp] for i in range(sn)).view(64, 48) if sn > 1 else sa
     na, nn, np_ = nt.rs_gemm(64, 48, torch.float32, fn)
-    res.append((axis, "rs", (ssum - na).abs().max().item(), na.abs().max().item()))
+    # (G > 2: NCCL's ring adds the members' partials in another order than the peer-memory
+    # epilogue's member order, so equality is to fp32 rounding, not bitwise)
+    tol = 0.0 if G <= 2 else 1e-6
+    res.append((axis, "rs", (ssum - na).abs().max().item(), na.abs().max().item(), tol))
+    # q-sub-chunked reduce-scatter (R > C grids: G / q gathered planes, each split into q owner
+    # chunks): batch j of sub-GEMM s goes to owner j*q + s
+    for q in sorted({v for v in (2, G) if G % v == 0 and v > 1}):
+        Aq = torch.randn((G // q) * 32 * q, 96, device=dev).bfloat16()
+
+        def fnq(s, D, d_bs, dpl, q=q, Aq=Aq):
+            K.gemm(D, Aq[s * 32:], Bm, 0, 0, 32, 48, 96, G // q, q * 32 * 96, 0, d_bs=d_bs, d_planes=dpl)
+
+        sa, sn, sp = st.rs_gemm(32, 48, torch.float32, fnq, q=q)
+        ssum = sum(sa.reshape(-1)[i * sp:(i + 1) * sp] for i in range(sn)).view(32, 48) if sn > 1 else sa
+        na, nn, np_ = nt.rs_gemm(32, 48, torch.float32, fnq, q=q)
+        res.append((axis, f"rs_q{q}", (ssum - na).abs().max().item(), na.abs().max().item(), tol))
     # GEMM + reduce-scatter + epilogue in one kernel (rs_gemm_fused) == GEMM -> barrier -> jg_epilogue,
     # bit for bit: multi-tile 2-CTA shapes, fp32 and bf16 partials, plain sum and bias + GELU epilogue
     rows, cols, kk = 512, 384, 256
@@ -64,7 +79,7 @@ for axis in ("row", "col"):
                 res.append((axis, f"rs_fused_{str(pdt)[6:]}_{epi}_{rep}", err, ref_d.abs().max().item()))
     torch.cuda.synchronize()
 print(rank, res, flush=True)
-bad = [r for r in res if r[2] != 0.0]
+bad = [r for r in res if r[2] > (r[4] * max(1.0, r[3]) if len(r) > 4 else 0.0)]
 if rank == 0:
     print("TRANSPORT_OK" if not bad else f"TRANSPORT_BAD {bad}", flush=True)
 dist.barrier()
