@@ -81,7 +81,7 @@ class GridWorkspace:
         ps = 4
         row_scratch = max(M * nmax * ps, Tl * E * ps)
         kin_max = max(E * Fl, H * El, E * Hl, F * El)
-        col_scratch = max(E * Kl * ps, kin_max * ps)
+        col_scratch = max(B * E * Kl * ps, kin_max * ps)  # token layers: all B samples' partials in one region
         kind = os.environ.get("JIGSAW_TRANSPORT", "symm" if dev.type == "cuda" else "nccl")
         if kind == "symm":
             self.row = SymmTransport(ctx.row_group, C, m.c, dev, row_scratch, row_persist) if C > 1 else None
@@ -317,6 +317,111 @@ def tok1_bwd(m, g, ws, j, bi, b, ghcol):
     K.gemm(out, urow, ghcol, KM, MN, Tl, Kl, El, C, B * Tl * El, El * Kl, reduce_batch=True, **kw)
 
 
+# ------------------------------------------------ token layers, all B samples per exchange
+# The token-mixing GEMMs run per sample (weight-first / transposed products of one sample's
+# tiles), but their exchanges do not need a barrier each: every sample's GEMM stores its
+# partial planes into its own part of one reduce-scatter region and its gathered output into
+# its own sub-slot, and ONE barrier per layer publishes all B samples (rs_gemm_multi /
+# publish_all) — B times fewer device barriers than a reduce-scatter per sample.
+def tok1_fwd_all(m, g, ws, j, b, uall):
+    """tok1_fwd for every sample; uall [C, B, Tl, El] (the row-gathered u). Returns the gelu(h)
+    operands of tok2 per sample."""
+    B = ws.B
+    if m.R == 1 or g.fused:
+        return [tok1_fwd(m, g, ws, j, bi, b, uall[:, bi]) for bi in range(B)]
+    p = m.params
+    Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
+    C, q, ps = m.C, g.q, B * Tl * El
+    fns, has = [], []
+    for bi in range(B):
+        urow = uall[:, bi]
+
+        def fn(s, D, d_bs, dpl, urow=urow, **kw):
+            K.gemm(D, urow[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
+                   d_planes=dpl, lda=El, **kw)
+        fns.append(fn)
+        has.append(g.col.dest((Er, Kl), m.op_dtype, slot=f"a_col{j}", sub=bi, nsub=B))
+    for bi, (acc, npl, pst) in enumerate(g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q)):
+        K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data,
+                   d=ws.h[j][bi], d2=has[bi].own, d2_bcast=has[bi].peers)
+    g.col.publish_all(has)
+    return [ha.planes.view(-1, Kl) for ha in has]
+
+
+def tok2_fwd_all(m, g, ws, j, b, acols):
+    B = ws.B
+    if g.fused or B == 1:
+        for bi in range(B):
+            tok2_fwd(m, g, ws, j, bi, b, acols[bi])
+        return
+    p, C = m.params, m.C
+    Tl, El, Kl = ws.Tl, ws.El, ws.Kl
+    fns = []
+    for bi in range(B):
+        def fn(s, D, d_bs, dpl, acol=acols[bi], **kw):
+            K.gemm(D, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
+        fns.append(fn)
+    for bi, (acc, npl, ps) in enumerate(g.row.rs_gemm_multi(Tl, El, g.pdt, fns)):
+        K.epilogue(acc, Tl, El, acc_bs=ps, nplanes=npl, epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data,
+                   resid=ws.res[j][bi], d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
+
+
+def tok2_bwd_all(m, g, ws, j, b, xall, acols):
+    """tok2_bwd for every sample: gh reduce-scatters over the column group (one barrier), gh
+    pushed back out over it (one barrier), then the dW2 GEMMs. Returns (gh local, gh gathered)
+    per sample."""
+    B = ws.B
+    if m.R == 1 or g.fused or B == 1:
+        return [tok2_bwd(m, g, ws, j, bi, b, xall[:, bi], acols[bi]) for bi in range(B)]
+    p = m.params
+    Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
+    C, q, ps = m.C, g.q, B * Tl * El
+    fns, hgs = [], []
+    for bi in range(B):
+        grow = xall[:, bi]
+
+        def fn(s, D, d_bs, dpl, grow=grow, **kw):
+            K.gemm(D, grow[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
+                   d_planes=dpl, lda=El, **kw)
+        fns.append(fn)
+        hgs.append(g.col.dest((Er, Kl), m.op_dtype, slot="gh_col", sub=bi, nsub=B))
+    for bi, (acc, npl, pst) in enumerate(g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q)):
+        K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_GB, pre=ws.h[j][bi], d=hgs[bi].own,
+                   d_bcast=hgs[bi].peers)
+    g.col.publish_all(hgs)
+    for bi in range(B):
+        out, kw = m._wgrad(b + "tok2.w") if bi == 0 else (p[b + "tok2.w"].grad, {"epi": E_ACC})
+        if bi == 0 and kw.get("epi") == _lib.EPI_ADAM:
+            out, kw = p[b + "tok2.w"].grad, {"epi": E_ACC}
+        K.gemm(out, xall[:, bi], acols[bi], KM, MN, Tl, Kl, El, C, ps, El * Kl, reduce_batch=True, **kw)
+    return [(hg.own, hg.planes.view(-1, Kl)) for hg in hgs]
+
+
+def tok1_bwd_all(m, g, ws, j, b, ghcols):
+    B = ws.B
+    if g.fused or B == 1:
+        for bi in range(B):
+            tok1_bwd(m, g, ws, j, bi, b, ghcols[bi])
+        return
+    p, C = m.params, m.C
+    Tl, El, Kl = ws.Tl, ws.El, ws.Kl
+    fns = []
+    for bi in range(B):
+        def fn(s, D, d_bs, dpl, ghcol=ghcols[bi], **kw):
+            K.gemm(D, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
+        fns.append(fn)
+    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, outs=[ws.gu[bi] for bi in range(B)])
+    for bi, (acc, npl, ps) in enumerate(res):
+        if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
+            K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
+    for bi in range(B):
+        urow = g.row.persistent(f"u_row{j}").view(C, B, Tl, El)[:, bi]
+        out, kw = m._wgrad(b + "tok1.w") if bi == 0 else (p[b + "tok1.w"].grad, {"epi": E_ACC})
+        if bi == 0 and kw.get("epi") == _lib.EPI_ADAM:
+            out, kw = p[b + "tok1.w"].grad, {"epi": E_ACC}
+        K.gemm(out, urow, ghcols[bi], KM, MN, Tl, Kl, El, C, B * Tl * El, El * Kl, reduce_batch=True, **kw)
+
+
 # --------------------------------------------------------------------------- forward / backward
 def forward_grid(m, ws) -> None:
     g = _gw(m, ws)
@@ -345,9 +450,8 @@ def forward_grid(m, ws) -> None:
                    M, El, E, m.eps, bcast=hu.peers)
         g.row.publish(hu)
         uall = hu.planes.view(C, B, Tl, El)
-        for bi in range(B):
-            acol = tok1_fwd(m, g, ws, j, bi, b, uall[:, bi])
-            tok2_fwd(m, g, ws, j, bi, b, acol)
+        acols = tok1_fwd_all(m, g, ws, j, b, uall)
+        tok2_fwd_all(m, g, ws, j, b, acols)
         ctx.all_reduce_row(ws.st2[j])
         K.ln_apply(ws.x2[j], ws.st2[j], p[b + "ln2.gamma"].data, p[b + "ln2.beta"].data, ws.v[j], ws.mr2[j],
                    M, El, E, m.eps)
@@ -400,14 +504,11 @@ def backward_grid(m, ws) -> None:
         g.row.publish(hx)
         xall = hx.planes.view(m.C, B, Tl, El)
         acol_all = g.col.persistent(f"a_col{j}").view(B, -1, Kl) if m.R > 1 else None
-        ghcols = []
-        for bi in range(B):
-            acol = acol_all[bi] if m.R > 1 else ws.a[j][bi]
-            gh_local, ghcol = tok2_bwd(m, g, ws, j, bi, b, xall[:, bi], acol)
+        acols = [acol_all[bi] if m.R > 1 else ws.a[j][bi] for bi in range(B)]
+        ghs = tok2_bwd_all(m, g, ws, j, b, xall, acols)
+        for gh_local, _ in ghs:
             K.colsum(gh_local, p[b + "tok1.b"].grad, Er, Kl)
-            ghcols.append(ghcol)
-        for bi in range(B):
-            tok1_bwd(m, g, ws, j, bi, b, ghcols[bi])
+        tok1_bwd_all(m, g, ws, j, b, [ghcol for _, ghcol in ghs])
         hg = g.row.dest((M, El), od, slot="g")                  # g operand copy -> row group
         # (same pass: column sums of g = the bias gradient of the previous block's ch2 / the encoder)
         nxt = f"block{(j - 1) % cfg.n_blocks}.ch2.b" if j > 0 else "enc.b"

@@ -87,7 +87,7 @@ class NcclTransport:
         for s_ in shape:
             n *= s_
         planes = self._slot(slot, nsub * self.G * n, dtype).view(nsub, self.G, *shape)[sub]
-        return Gather(planes, self._buf(("own", slot), n, dtype).view(*shape), [])
+        return Gather(planes, self._buf(("own", slot, sub), n, dtype).view(*shape), [])
 
     def publish(self, h: Gather) -> None:
         self.bytes_sent += (self.G - 1) * h.own.numel() * h.own.element_size()
@@ -96,18 +96,27 @@ class NcclTransport:
         else:
             dist.all_gather_into_tensor(h.planes.view(-1), h.own.reshape(-1), group=self.group)
 
-    def rs_gemm(self, rows: int, cols: int, dtype, fn, q: int = 1, out: torch.Tensor | None = None):
+    def rs_gemm(self, rows: int, cols: int, dtype, fn, q: int = 1, out: torch.Tensor | None = None, key: int = 0):
         """fn(s, D, d_bs, d_planes) for s < q computes GEMM batches j writing owner plane j*q + s."""
-        planes = self._buf("rs", self.G * rows * cols, dtype).view(self.G, rows, cols)
+        planes = self._buf(("rs", key), self.G * rows * cols, dtype).view(self.G, rows, cols)
         for s in range(q):
             fn(s, planes[s], q * rows * cols, None)
         self.bytes_sent += (self.G - 1) * rows * cols * planes.element_size()
         if self.G == 1:
             return planes[0], 1, 0
         use_out = out is not None and out.dtype == dtype
-        red = out if use_out else self._buf("red", rows * cols, dtype).view(rows, cols)
+        red = out if use_out else self._buf(("red", key), rows * cols, dtype).view(rows, cols)
         dist.reduce_scatter_tensor(red.view(-1), planes.view(-1), group=self.group)
         return red, 1, 0
+
+    def rs_gemm_multi(self, rows: int, cols: int, dtype, fns, q: int = 1, outs=None):
+        """Several independent reduce-scatters of the same shape (e.g. one per sample)."""
+        outs = outs or [None] * len(fns)
+        return [self.rs_gemm(rows, cols, dtype, fn, q, out=o, key=k) for k, (fn, o) in enumerate(zip(fns, outs))]
+
+    def publish_all(self, hs) -> None:
+        for h in hs:
+            self.publish(h)
 
 
 FLAG_CAP = 1 << 15  # arrival counters per reduce-scatter region (jg_gemm_desc.rs_flag_cap)
@@ -230,6 +239,31 @@ class SymmTransport:
         self.bytes_sent += (self.G - 1) * pbytes
         self.barrier()
         return local, self.G, rows * cols
+
+    def rs_gemm_multi(self, rows: int, cols: int, dtype, fns, q: int = 1, outs=None):
+        """Several independent reduce-scatters of one shape (the B samples of a token layer): every
+        GEMM stores its partial planes into its own part of one region, then ONE barrier
+        publishes them all — B times fewer barriers than a reduce-scatter per sample."""
+        es = torch.empty((), dtype=dtype).element_size()
+        pbytes = rows * cols * es
+        off = self._region()
+        assert len(fns) * self.G * pbytes <= self.scratch_bytes, "reduce-scatter region too small"
+        res = []
+        for k, fn in enumerate(fns):
+            ko = off + k * self.G * pbytes
+            local = self._view(ko, (self.G, rows, cols), dtype)
+            for s in range(q):
+                fn(s, local[0], 0, [self.base[j * q + s] + ko + self.idx * pbytes for j in range(self.G // q)])
+            self.bytes_sent += (self.G - 1) * pbytes
+            res.append((local, self.G, rows * cols))
+        self.barrier()
+        return res
+
+    def publish_all(self, hs) -> None:
+        """One barrier publishes several producer-pushed gathers."""
+        for h in hs:
+            self.bytes_sent += len(h.peers) * h.own.numel() * h.own.element_size()
+        self.barrier()
 
     def rs_gemm_fused(self, rows: int, cols: int, dtype, fn, q: int = 1, **epi) -> None:
         """Reduce-scatter fused into the GEMM (jg_gemm_desc rs_*): each launch stores its
