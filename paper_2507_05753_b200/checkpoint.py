@@ -10,7 +10,9 @@ One file per model-parallel position, shards never merged:
                u32 ndim, ndim x u64 dims, payload (C order)
 
 Records: param/<name> (fp32 master), adam_m/<name>, adam_v/<name>, step (int32 Adam counter =
-schedule position). Loading checks format, world shape and model-config hash and restores
+schedule position). A Trainer checkpoint adds a "trainer" header entry: the epoch, the batches of
+it already trained and the rollout RNG's epoch-start state, so a resumed fine-tuning run draws
+the same rollouts and samples as the uninterrupted one. Loading checks format, world shape and model-config hash and restores
 bit-identical parameters, moments and step; the bf16 operand copies are re-derived. Within a
 data-parallel group every replica holds the same shard, so only dp index 0 writes.
 """
@@ -43,16 +45,19 @@ def _records(step) -> list[tuple[str, np.ndarray]]:
     return [(k, t.detach().cpu().numpy()) for k, t in out]
 
 
-def _header(step, nrec: int) -> dict:
+def _header(step, nrec: int, extra: dict | None = None) -> dict:
     m = step.model
-    return {"format": FORMAT, "version": VERSION, "rank": m.ctx.pos, "n": m.ctx.n, "grid": [m.R, m.C],
-            "config_hash": m.cfg.content_hash(), "op_dtype": str(m.op_dtype).replace("torch.", ""),
-            "step": int(step.step_count.item()), "records": nrec}
+    h = {"format": FORMAT, "version": VERSION, "rank": m.ctx.pos, "n": m.ctx.n, "grid": [m.R, m.C],
+         "config_hash": m.cfg.content_hash(), "op_dtype": str(m.op_dtype).replace("torch.", ""),
+         "step": int(step.step_count.item()), "records": nrec}
+    h.update(extra or {})
+    return h
 
 
-def save(step, directory: str) -> str | None:
-    """Write this rank's shard (TrainStep state: master weights, Adam moments, step counter).
-    Returns the file written, or None on dp replicas other than index 0."""
+def save(step, directory: str, extra: dict | None = None) -> str | None:
+    """Write this rank's shard (TrainStep state: master weights, Adam moments, step counter; `extra`
+    header fields, e.g. the Trainer's epoch / position / rollout-RNG state). Returns the file
+    written, or None on dp replicas other than index 0."""
     if step.model.ctx.dp_index != 0:
         return None
     if step.model.device.type == "cuda":
@@ -62,7 +67,7 @@ def save(step, directory: str) -> str | None:
     path = shard_path(directory, step.model.ctx.pos, step.model.ctx.n)
     tmp = path + ".tmp"
     with open(tmp, "wb") as fh:
-        fh.write((json.dumps(_header(step, len(recs)), sort_keys=True) + "\n").encode())
+        fh.write((json.dumps(_header(step, len(recs), extra), sort_keys=True) + "\n").encode())
         for name, a in recs:
             a = np.ascontiguousarray(a)
             dt = a.dtype.newbyteorder("<")

@@ -80,10 +80,11 @@ class TileLoader:
             self.read_tile(int(i), xn[b])
             self.read_tile(int(i) + lead, tn[b])
 
-    def epoch(self, epoch: int = 0, leads=None):
+    def epoch(self, epoch: int = 0, leads=None, start: int = 0):
         """Yields pinned (x, target) batches; a background thread reads ahead into free slots.
         A yielded pair stays valid until the next item is requested. `leads[s]` (<= lead) is
-        batch s's target lead (rollout fine-tuning), default `lead`."""
+        batch s's target lead (rollout fine-tuning), default `lead`. `start`: skip the epoch's
+        first batches (resuming from a mid-epoch checkpoint)."""
         ids = self.order(epoch)
         if leads is not None and max(leads, default=0) > self.lead:
             raise ConfigError(f"target lead {max(leads)} exceeds the loader's lead {self.lead}")
@@ -94,7 +95,7 @@ class TileLoader:
         stop = threading.Event()
 
         def work():
-            for s in range(nb):
+            for s in range(start, nb):
                 k = free.get()
                 if stop.is_set():
                     return
@@ -109,7 +110,7 @@ class TileLoader:
         th = threading.Thread(target=work, daemon=True)
         th.start()
         try:
-            for _ in range(nb):
+            for _ in range(max(0, nb - start)):
                 k = ready.get()
                 if isinstance(k, BaseException):
                     raise k

@@ -323,6 +323,10 @@ class Trainer:
         self.rng = np.random.default_rng(seed)
         self.step_count = torch.zeros(1, dtype=torch.int32, device=model.device)
         self.steps: dict[int, TrainStep] = {}
+        # position for checkpoint / resume: the epoch in progress, the batches of it already
+        # trained, and the rollout RNG state from before that epoch's draws
+        self.epoch, self.step_in_epoch = 0, 0
+        self._epoch_rng_state = self.rng.bit_generator.state
 
     def step_for(self, r: int) -> TrainStep:
         if r not in self.steps:
@@ -335,25 +339,50 @@ class Trainer:
             return np.ones(n, dtype=np.int64)
         return self.rng.integers(1, self.r_max + 1, size=n)
 
-    def train_epoch(self, loader, epoch: int = 0, max_steps: int | None = None) -> dict:
+    def train_epoch(self, loader, epoch: int = 0, max_steps: int | None = None, start: int = 0) -> dict:
         """One pass over this replica's share of the samples; returns mean loss, per-step losses
-        and rollouts, and the wall time."""
+        and rollouts, and the wall time. `start`: batches of this epoch already trained (resume;
+        the RNG must hold the epoch-start state, as load_checkpoint restores it)."""
         import time
-        nb = loader.steps_per_epoch() if max_steps is None else min(max_steps, loader.steps_per_epoch())
+        nb = loader.steps_per_epoch() if max_steps is None else min(start + max_steps, loader.steps_per_epoch())
         if (loader.lat_real, loader.vars_real) != (self.model.lat_real, self.model.vars_real):
             raise ConfigError(f"loader data is {loader.lat_real} rows x {loader.vars_real} channels but the model's "
                               f"loss mask is {self.model.lat_real} x {self.model.vars_real}: build the model with "
                               f"lat_real=loader.lat_real, vars_real=loader.vars_real")
-        rs = self.draw_rollouts(nb)
+        self._epoch_rng_state = self.rng.bit_generator.state
+        self.epoch, self.step_in_epoch = epoch, start
+        rs = self.draw_rollouts(loader.steps_per_epoch())
         if self.r_max > 1 and loader.lead < self.r_max:
             raise ConfigError(f"loader lead {loader.lead} < r_max {self.r_max}: build it with lead=r_max")
         losses = []
         t0 = time.perf_counter()
-        for s, (x, t) in enumerate(loader.epoch(epoch, leads=rs if self.r_max > 1 else None)):
+        for s, (x, t) in enumerate(loader.epoch(epoch, leads=rs if self.r_max > 1 else None, start=start), start):
             if s >= nb:
                 break
             losses.append(self.step_for(int(rs[s]))(x, t))
+            self.step_in_epoch = s + 1
         return {"loss": float(np.mean(losses)) if losses else float("nan"), "losses": losses,
-                "rollouts": rs[:len(losses)].tolist(), "seconds": time.perf_counter() - t0}
+                "rollouts": rs[start:start + len(losses)].tolist(), "seconds": time.perf_counter() - t0}
+
+    def save_checkpoint(self, directory: str) -> str | None:
+        """This rank's shard (weights, Adam state, step) plus the training position: epoch, batches
+        done in it, and the rollout RNG's epoch-start state."""
+        from . import checkpoint
+        step = next(iter(self.steps.values()), None) or self.step_for(1)
+        return checkpoint.save(step, directory, extra={"trainer": {
+            "epoch": self.epoch, "step_in_epoch": self.step_in_epoch, "rng_state": self._epoch_rng_state}})
+
+    def load_checkpoint(self, directory: str) -> tuple[int, int]:
+        """Restore a shard written by save_checkpoint; returns (epoch, start) for train_epoch, which
+        then reproduces the uninterrupted run (same rollout draws, same samples)."""
+        from . import checkpoint
+        header = checkpoint.load(self.step_for(1), directory)
+        tr = header.get("trainer")
+        if tr is None:
+            return 0, 0
+        self.rng.bit_generator.state = tr["rng_state"]
+        self._epoch_rng_state = tr["rng_state"]
+        self.epoch, self.step_in_epoch = int(tr["epoch"]), int(tr["step_in_epoch"])
+        return self.epoch, self.step_in_epoch
 
     finetune_rollout = train_epoch

@@ -122,6 +122,32 @@ def _worker(rank, world, port, out_q, r, mode="fwdbwd", opts=None):
                 dist.barrier()
                 dist.destroy_process_group()
             return
+        if mode == "resume":
+            # a fine-tuning run interrupted after 2 batches and resumed from its checkpoint by a
+            # fresh Trainer (other init) reproduces the uninterrupted run: same rollout draws,
+            # same samples, same losses and weights
+            from paper_2507_05753_b200.data import TileLoader
+            from paper_2507_05753_b200.engine import Trainer
+            src = np.random.default_rng(7).standard_normal((7, *oc.grid, oc.n_vars)).astype(np.float32)
+            ld = TileLoader(src, cfg, ctx, lead=2, batch=1, seed=3)
+            full = Trainer(model, batch=1, r_max=2, seed=11, graph=False).train_epoch(ld, 0)
+            m2 = WeatherMixerModel(ctx, cfg, seed=0, dtype="f32", device="cpu")
+            t2 = Trainer(m2, batch=1, r_max=2, seed=11, graph=False)
+            first = t2.train_epoch(ld, 0, max_steps=2)
+            t2.save_checkpoint(opts["dir"])
+            m3 = WeatherMixerModel(ctx, cfg, seed=5, dtype="f32", device="cpu")
+            t3 = Trainer(m3, batch=1, r_max=2, seed=99, graph=False)
+            ep, start = t3.load_checkpoint(opts["dir"])
+            rest = t3.train_epoch(ld, ep, start=start)
+            out_q.put({"pos": ctx.pos, "rank": rank, "full": full["losses"], "rollouts": full["rollouts"],
+                       "resumed": first["losses"] + rest["losses"],
+                       "resumed_rollouts": first["rollouts"] + rest["rollouts"], "start": start,
+                       "same_params": all(torch.equal(model.params[k].data, m3.params[k].data) for k in model.params)})
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+                dist.destroy_process_group()
+            return
         if mode == "comm":
             # one step warms the panels, the second is the steady state: its transport / all-reduce
             # byte counters must equal the analytic per-step volume of the schedule
@@ -520,3 +546,15 @@ def test_comm_volume_matches_analytic(world, transport, dtype, grid):
         assert ex == d["analytic"]["exchange"], (d["pos"], ex, d["analytic"])
         assert abs(ar - d["analytic"]["allreduce"]) <= 1e-6 * max(1.0, ar), (d["pos"], ar, d["analytic"])
         assert ex > 0
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_trainer_resume_reproduces_uninterrupted_run(world, tmp_path):
+    """Trainer checkpoints carry the epoch, the position in it and the rollout RNG's epoch-start
+    state: resuming mid-epoch reproduces the uninterrupted fine-tuning run."""
+    res = _run(world, mode="resume", opts={"dir": str(tmp_path / "ck")})
+    for d in res:
+        assert d["start"] == 2
+        assert d["resumed_rollouts"] == d["rollouts"]
+        np.testing.assert_allclose(d["resumed"], d["full"], rtol=1e-6, atol=0)
+        assert d["same_params"]
