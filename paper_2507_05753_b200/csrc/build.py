@@ -47,27 +47,39 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, out: Path | None = None) -> Path:
+    """out: build a variant elsewhere (e.g. tools/variants/X.so, loaded with JIGSAW_LIB=...) without
+    touching the in-tree library or its flags stamp."""
+    if out is not None:
+        return _compile(Path(out), verbose, stamp=False)
     if not force and not _stale():
         return OUT
+    return _compile(OUT, verbose, stamp=True)
+
+
+def _compile(target: Path, verbose: bool, stamp: bool) -> Path:
     objs = []
     for src in SOURCES:
-        obj = HERE / (Path(src).stem + ".o")
+        obj = target.parent / (target.stem + "_" + Path(src).stem + ".o")
         cmd = [NVCC, *FLAGS, "-c", str(HERE / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = OUT.with_suffix(".so.tmp")
+    tmp = target.with_suffix(".so.tmp")
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs, "-lcudart"],
                    check=True)
-    os.replace(tmp, OUT)
-    STAMP.write_text(_flags_id())
+    os.replace(tmp, target)
+    if stamp:
+        STAMP.write_text(_flags_id())
     for o in objs:
         os.unlink(o)
-    return OUT
+    return target
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force=True))
+    # python -m paper_2507_05753_b200.csrc.build [--verbose] [--out tools/variants/X.so]  (JG_NVCC_EXTRA=...)
+    args = sys.argv[1:]
+    out = Path(args[args.index("--out") + 1]) if "--out" in args else None
+    print(build(verbose="--verbose" in args, force=True, out=out))

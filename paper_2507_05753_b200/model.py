@@ -584,7 +584,7 @@ class WeatherMixerModel:
             # fp32 mode: the kernel's operand copy is bf16-only; copy (and push) the fp32 result
             K.ln_bwd_apply(x, gin, p[pre + "gamma"].data, mr, bst, resid, out, None, p[pre + "gamma"].grad,
                            p[pre + "beta"].grad, rows, cols, c_total, **(sums or {}))
-            out_op.view(-1).copy_(out.view(-1))
+            K.copy_async(out_op.data_ptr(), out, out.numel() * 4)
             for addr in bcast or []:
                 K.copy_async(addr, out, out.numel() * 4)
             return

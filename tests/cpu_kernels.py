@@ -50,6 +50,10 @@ def _bcast_copy(src, addrs):
 
 def copy_async(dst_ptr, src, nbytes=None):
     nbytes = src.numel() * src.element_size() if nbytes is None else nbytes
+    if not any(base <= dst_ptr < base + n for base, n, _ in _PEERS):  # a local (host) buffer
+        import ctypes
+        ctypes.memmove(dst_ptr, src.contiguous().data_ptr(), nbytes)
+        return
     _at(dst_ptr, torch.uint8, (nbytes,), (1,)).copy_(src.contiguous().view(-1).view(torch.uint8)[:nbytes])
 
 
