@@ -58,7 +58,7 @@ def timed(step, n=10):
 variants = sys.argv[1:] or ["base", "nobarrier", "noar", "nocopy", "noepilogue", "nocomm"]
 for v in variants:
     apply(v)
-    step = TrainStep(model)
+    step = TrainStep(model, batch=int(os.environ.get("B", "1")))
     bench.fill_random_inputs(step, lat_real, 1234 + ctx.pos)
     step.capture()
     restore()

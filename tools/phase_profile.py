@@ -11,7 +11,7 @@ comm = Communicator.from_env()
 ctx = MpContext(comm, list(range(comm.world_size)))
 cfg_kw, lat_real, vars_real, _ = bench.CONFIGS[os.environ.get("CFG", "C4")]
 model = WeatherMixerModel(ctx, ModelConfig(**cfg_kw), init="fast", lat_real=lat_real, vars_real=vars_real)
-step = TrainStep(model, graph=False)
+step = TrainStep(model, batch=int(os.environ.get("B", "1")), graph=False)
 bench.fill_random_inputs(step, lat_real, 1234 + ctx.pos)
 recs = collections.defaultdict(list)
 
