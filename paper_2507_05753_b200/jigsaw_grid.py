@@ -39,7 +39,7 @@ import torch
 
 from . import _lib
 from . import kernels as K
-from .transport import NcclTransport, SymmTransport, fused_rs_enabled
+from .transport import Fanout, NcclTransport, SymmTransport, fused_rs_enabled
 
 KM, MN = _lib.JG_KMAJOR, _lib.JG_MNMAJOR
 E_ACC, E_BCOL, E_BROW, E_RES = _lib.EPI_ACCUM, _lib.EPI_BIAS_COL, _lib.EPI_BIAS_ROW, _lib.EPI_RESID
@@ -105,6 +105,8 @@ class GridWorkspace:
         bf = od == torch.bfloat16 and os.environ.get("JIGSAW_PARTIALS", "bf16") != "fp32"
         self.pdt = torch.bfloat16 if bf else F32
         self.dgrad = torch.empty(max(kin_max, E * Kl), dtype=F32, device=dev)  # reduced weight gradients
+        # per-sample token GEMMs of a B > 1 step run side by side on a few side streams
+        self.fan = Fanout(dev, min(B, int(os.environ.get("JIGSAW_FANOUT", "4"))))
         self.panels = {n: self.col.persistent(f"panel:{n}").view(panel_shape[_base(n)]) for n in self.panel_names}
         # live buffers of received parameter blocks (reference MpContext.param_buffer_peak,
         # parallel.py:71-76): the peers' planes of every gathered weight panel, held for the step
@@ -327,8 +329,11 @@ def tok1_fwd_all(m, g, ws, j, b, uall):
     """tok1_fwd for every sample; uall [C, B, Tl, El] (the row-gathered u). Returns the gelu(h)
     operands of tok2 per sample."""
     B = ws.B
-    if m.R == 1 or g.fused:
+    if g.fused:
         return [tok1_fwd(m, g, ws, j, bi, b, uall[:, bi]) for bi in range(B)]
+    if m.R == 1:  # local GEMMs, one per sample, side by side
+        g.fan([lambda bi=bi: tok1_fwd(m, g, ws, j, bi, b, uall[:, bi]) for bi in range(B)])
+        return [ws.a[j][bi] for bi in range(B)]
     p = m.params
     Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
     C, q, ps = m.C, g.q, B * Tl * El
@@ -341,9 +346,10 @@ def tok1_fwd_all(m, g, ws, j, b, uall):
                    d_planes=dpl, lda=El, **kw)
         fns.append(fn)
         has.append(g.col.dest((Er, Kl), m.op_dtype, slot=f"a_col{j}", sub=bi, nsub=B))
-    for bi, (acc, npl, pst) in enumerate(g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q)):
-        K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data,
-                   d=ws.h[j][bi], d2=has[bi].own, d2_bcast=has[bi].peers)
+    res = g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q, run=g.fan)
+    g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Er, Kl, acc_bs=r[2], nplanes=r[1], epi=E_BCOL | E_GF,
+                                         bias=p[b + "tok1.b"].data, d=ws.h[j][bi], d2=has[bi].own,
+                                         d2_bcast=has[bi].peers) for bi, r in enumerate(res)])
     g.col.publish_all(has)
     return [ha.planes.view(-1, Kl) for ha in has]
 
@@ -361,9 +367,10 @@ def tok2_fwd_all(m, g, ws, j, b, acols):
         def fn(s, D, d_bs, dpl, acol=acols[bi], **kw):
             K.gemm(D, p[b + "tok2.w"].op, acol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
         fns.append(fn)
-    for bi, (acc, npl, ps) in enumerate(g.row.rs_gemm_multi(Tl, El, g.pdt, fns)):
-        K.epilogue(acc, Tl, El, acc_bs=ps, nplanes=npl, epi=E_BROW | E_RES | E_ST, bias=p[b + "tok2.b"].data,
-                   resid=ws.res[j][bi], d=ws.x2[j][bi], stats=ws.st2[j][bi * Tl:(bi + 1) * Tl])
+    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, run=g.fan)
+    g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Tl, El, acc_bs=r[2], nplanes=r[1], epi=E_BROW | E_RES | E_ST,
+                                         bias=p[b + "tok2.b"].data, resid=ws.res[j][bi], d=ws.x2[j][bi],
+                                         stats=ws.st2[j][bi * Tl:(bi + 1) * Tl]) for bi, r in enumerate(res)])
 
 
 def tok2_bwd_all(m, g, ws, j, b, xall, acols):
@@ -371,11 +378,17 @@ def tok2_bwd_all(m, g, ws, j, b, xall, acols):
     pushed back out over it (one barrier), then the dW2 GEMMs. Returns (gh local, gh gathered)
     per sample."""
     B = ws.B
-    if m.R == 1 or g.fused or B == 1:
+    if g.fused or B == 1:
         return [tok2_bwd(m, g, ws, j, bi, b, xall[:, bi], acols[bi]) for bi in range(B)]
     p = m.params
     Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
     C, q, ps = m.C, g.q, B * Tl * El
+    if m.R == 1:
+        # gh = (g_x2^T W2) * gelu'(h), local, one GEMM per sample side by side
+        g.fan([lambda bi=bi: K.gemm(ws.gh[bi], xall[:, bi], p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C, ps, 0,
+                                    d_bs=El * Kl, epi=E_GB, pre=ws.h[j][bi]) for bi in range(B)])
+        _dw_tok2(m, ws, b, xall, acols)
+        return [(ws.gh[bi], ws.gh[bi]) for bi in range(B)]
     fns, hgs = [], []
     for bi in range(B):
         grow = xall[:, bi]
@@ -385,16 +398,23 @@ def tok2_bwd_all(m, g, ws, j, b, xall, acols):
                    d_planes=dpl, lda=El, **kw)
         fns.append(fn)
         hgs.append(g.col.dest((Er, Kl), m.op_dtype, slot="gh_col", sub=bi, nsub=B))
-    for bi, (acc, npl, pst) in enumerate(g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q)):
-        K.epilogue(acc, Er, Kl, acc_bs=pst, nplanes=npl, epi=E_GB, pre=ws.h[j][bi], d=hgs[bi].own,
-                   d_bcast=hgs[bi].peers)
+    res = g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q, run=g.fan)
+    g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Er, Kl, acc_bs=r[2], nplanes=r[1], epi=E_GB, pre=ws.h[j][bi],
+                                         d=hgs[bi].own, d_bcast=hgs[bi].peers) for bi, r in enumerate(res)])
     g.col.publish_all(hgs)
+    _dw_tok2(m, ws, b, xall, acols)
+    return [(hg.own, hg.planes.view(-1, Kl)) for hg in hgs]
+
+
+def _dw_tok2(m, ws, b, xall, acols):
+    """dW2 = sum_b g_x2[b] a[b]: the samples accumulate into one gradient, so in order."""
+    p, C, B = m.params, m.C, ws.B
+    Tl, El, Kl = ws.Tl, ws.El, ws.Kl
     for bi in range(B):
         out, kw = m._wgrad(b + "tok2.w") if bi == 0 else (p[b + "tok2.w"].grad, {"epi": E_ACC})
         if bi == 0 and kw.get("epi") == _lib.EPI_ADAM:
             out, kw = p[b + "tok2.w"].grad, {"epi": E_ACC}
-        K.gemm(out, xall[:, bi], acols[bi], KM, MN, Tl, Kl, El, C, ps, El * Kl, reduce_batch=True, **kw)
-    return [(hg.own, hg.planes.view(-1, Kl)) for hg in hgs]
+        K.gemm(out, xall[:, bi], acols[bi], KM, MN, Tl, Kl, El, C, B * Tl * El, El * Kl, reduce_batch=True, **kw)
 
 
 def tok1_bwd_all(m, g, ws, j, b, ghcols):
@@ -410,10 +430,9 @@ def tok1_bwd_all(m, g, ws, j, b, ghcols):
         def fn(s, D, d_bs, dpl, ghcol=ghcols[bi], **kw):
             K.gemm(D, p[b + "tok1.w"].op, ghcol, KM, KM, Tl, El, Kl, C, 0, El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
         fns.append(fn)
-    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, outs=[ws.gu[bi] for bi in range(B)])
-    for bi, (acc, npl, ps) in enumerate(res):
-        if npl > 1 or acc.data_ptr() != ws.gu[bi].data_ptr():
-            K.sum_planes(ws.gu[bi], acc, Tl * El, npl, ps)
+    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, outs=[ws.gu[bi] for bi in range(B)], run=g.fan)
+    g.fan([lambda bi=bi, r=r: K.sum_planes(ws.gu[bi], r[0], Tl * El, r[1], r[2]) for bi, r in enumerate(res)
+           if r[1] > 1 or r[0].data_ptr() != ws.gu[bi].data_ptr()])
     for bi in range(B):
         urow = g.row.persistent(f"u_row{j}").view(C, B, Tl, El)[:, bi]
         out, kw = m._wgrad(b + "tok1.w") if bi == 0 else (p[b + "tok1.w"].grad, {"epi": E_ACC})

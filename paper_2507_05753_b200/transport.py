@@ -109,10 +109,25 @@ class NcclTransport:
         dist.reduce_scatter_tensor(red.view(-1), planes.view(-1), group=self.group)
         return red, 1, 0
 
-    def rs_gemm_multi(self, rows: int, cols: int, dtype, fns, q: int = 1, outs=None):
-        """Several independent reduce-scatters of the same shape (e.g. one per sample)."""
+    def rs_gemm_multi(self, rows: int, cols: int, dtype, fns, q: int = 1, outs=None, run=None):
+        """Several independent reduce-scatters of the same shape (e.g. one per sample). `run`
+        launches a list of closures (e.g. concurrently on side streams); then one NCCL
+        reduce-scatter per item."""
         outs = outs or [None] * len(fns)
-        return [self.rs_gemm(rows, cols, dtype, fn, q, out=o, key=k) for k, (fn, o) in enumerate(zip(fns, outs))]
+        planes = [self._buf(("rs", k), self.G * rows * cols, dtype).view(self.G, rows, cols) for k in range(len(fns))]
+        calls = [lambda fn=fn, pl=pl, s=s: fn(s, pl[s], q * rows * cols, None)
+                 for fn, pl in zip(fns, planes) for s in range(q)]
+        (run or _run_all)(calls)
+        res = []
+        for k, (pl, o) in enumerate(zip(planes, outs)):
+            self.bytes_sent += (self.G - 1) * rows * cols * pl.element_size()
+            if self.G == 1:
+                res.append((pl[0], 1, 0))
+                continue
+            red = o if o is not None and o.dtype == dtype else self._buf(("red", k), rows * cols, dtype).view(rows, cols)
+            dist.reduce_scatter_tensor(red.view(-1), pl.reshape(-1), group=self.group)
+            res.append((red, 1, 0))
+        return res
 
     def publish_all(self, hs) -> None:
         for h in hs:
@@ -120,6 +135,36 @@ class NcclTransport:
 
 
 FLAG_CAP = 1 << 15  # arrival counters per reduce-scatter region (jg_gemm_desc.rs_flag_cap)
+
+
+def _run_all(calls) -> None:
+    for c in calls:
+        c()
+
+
+class Fanout:
+    """Launch independent closures concurrently on a few side streams forked from the current
+    stream and joined back into it (graph-capturable: the capture records the fork / join as
+    parallel branches). Used for the per-sample token-mixing GEMMs of a B > 1 grid step: each
+    alone has too few tiles to fill 148 SMs (C3 at 1x2: 16-32 tiles), side by side they do."""
+
+    def __init__(self, device, width: int):
+        self.cuda = device.type == "cuda" and width > 1
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(width)] if self.cuda else []
+
+    def __call__(self, calls) -> None:
+        if not self.cuda or len(calls) < 2:
+            _run_all(calls)
+            return
+        cur = torch.cuda.current_stream()
+        used = self.streams[:min(len(self.streams), len(calls))]
+        for s in used:
+            s.wait_stream(cur)
+        for i, c in enumerate(calls):
+            with torch.cuda.stream(used[i % len(used)]):
+                c()
+        for s in used:
+            cur.wait_stream(s)
 
 
 def fused_rs_enabled() -> bool:
@@ -240,22 +285,26 @@ class SymmTransport:
         self.barrier()
         return local, self.G, rows * cols
 
-    def rs_gemm_multi(self, rows: int, cols: int, dtype, fns, q: int = 1, outs=None):
+    def rs_gemm_multi(self, rows: int, cols: int, dtype, fns, q: int = 1, outs=None, run=None):
         """Several independent reduce-scatters of one shape (the B samples of a token layer): every
         GEMM stores its partial planes into its own part of one region, then ONE barrier
-        publishes them all — B times fewer barriers than a reduce-scatter per sample."""
+        publishes them all — B times fewer barriers than a reduce-scatter per sample. `run`
+        launches the GEMM closures (e.g. concurrently on side streams, so B small GEMMs fill the
+        GPU together)."""
         es = torch.empty((), dtype=dtype).element_size()
         pbytes = rows * cols * es
         off = self._region()
         assert len(fns) * self.G * pbytes <= self.scratch_bytes, "reduce-scatter region too small"
-        res = []
+        res, calls = [], []
         for k, fn in enumerate(fns):
             ko = off + k * self.G * pbytes
             local = self._view(ko, (self.G, rows, cols), dtype)
             for s in range(q):
-                fn(s, local[0], 0, [self.base[j * q + s] + ko + self.idx * pbytes for j in range(self.G // q)])
+                dpl = [self.base[j * q + s] + ko + self.idx * pbytes for j in range(self.G // q)]
+                calls.append(lambda fn=fn, local=local, s=s, dpl=dpl: fn(s, local[0], 0, dpl))
             self.bytes_sent += (self.G - 1) * pbytes
             res.append((local, self.G, rows * cols))
+        (run or _run_all)(calls)
         self.barrier()
         return res
 
