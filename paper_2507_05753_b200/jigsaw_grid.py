@@ -70,6 +70,7 @@ class GridWorkspace:
         self.panel_names = [n for n in m.params if _base(n) in CHANNEL_LAYERS] if R > 1 else []
         nmax = max(E, H, F)
         row_persist = [(f"u_row{j}", (C, B, Tl, El), od) for j in range(nj)]  # plane-major: LN writes its plane
+        row_persist += [("moments", (2, C, M, 2), F32)]  # layer-norm row moments, two alternating sub-slots
         row_persist += [("g", (C, M, El), od), ("gc", (C, M, Hl), od), ("gx2", (C, M, El), od), ("gd", (C, M, Fl), od),
                         ("tmp", (C, M, nmax // C), od)]
         col_persist = [("tmp", (R, max(E * Kl, max(E * Fl, H * El, E * Hl, F * El) // R)), od)]
@@ -98,6 +99,10 @@ class GridWorkspace:
                 for name, shape, dt in spec:
                     tr.reserve(name, shape, dt)
         self.kind = kind
+        # layer-norm row moments summed over the row group through peer memory (push + barrier +
+        # member-order plane sum) instead of an NCCL all-reduce
+        self.peer_moments = kind == "symm" and C > 1 and peer_moments_enabled()
+        self._mk = 0
         # GEMM + reduce-scatter + epilogue in one kernel (symmetric-memory transport, both axes)
         self.fused = kind == "symm" and fused_rs_enabled() and C > 1
         # reduce-scatter partial planes travel in the operand dtype (bf16 mode: half the NVLink bytes
@@ -112,6 +117,24 @@ class GridWorkspace:
         # parallel.py:71-76): the peers' planes of every gathered weight panel, held for the step
         held = sum(p.numel() * (R - 1) // R for p in self.panels.values())
         ctx.param_buffer_peak = max(ctx.param_buffer_peak, held)
+
+
+def peer_moments_enabled() -> bool:
+    return os.environ.get("JIGSAW_PEER_MOMENTS", "1") == "1"
+
+
+def row_reduce(m, g, t: torch.Tensor) -> torch.Tensor:
+    """Sum of a row-moment buffer [M, 2] over the row group (the grid form of the reference's
+    stats_peer exchange, model.py:220-231): every member pushes its partials into every member's
+    "moments" slot (copy engine), one barrier, then the planes are summed in member order — the
+    same bits on every member, no NCCL launch. NCCL all-reduce on the NCCL transport."""
+    if not g.peer_moments:
+        return m.ctx.all_reduce_row(t)
+    sub = g._mk % 2
+    g._mk += 1
+    planes = g.row.ag(t.view(-1), slot="moments", sub=sub, nsub=2)
+    K.sum_planes(t.view(-1), planes, t.numel(), m.C, t.numel())
+    return t
 
 
 def _gw(m, ws) -> GridWorkspace:
@@ -463,7 +486,7 @@ def forward_grid(m, ws) -> None:
     nj = ws.r * cfg.n_blocks
     for j in range(nj):
         b = f"block{j % cfg.n_blocks}."
-        ctx.all_reduce_row(ws.st1[j])
+        row_reduce(m, g, ws.st1[j])
         hu = g.row.dest((M, El), od, slot=f"u_row{j}")          # LN1 output pushed to the row group
         K.ln_apply(ws.res[j], ws.st1[j], p[b + "ln1.gamma"].data, p[b + "ln1.beta"].data, hu.own, ws.mr1[j],
                    M, El, E, m.eps, bcast=hu.peers)
@@ -471,7 +494,7 @@ def forward_grid(m, ws) -> None:
         uall = hu.planes.view(C, B, Tl, El)
         acols = tok1_fwd_all(m, g, ws, j, b, uall)
         tok2_fwd_all(m, g, ws, j, b, acols)
-        ctx.all_reduce_row(ws.st2[j])
+        row_reduce(m, g, ws.st2[j])
         K.ln_apply(ws.x2[j], ws.st2[j], p[b + "ln2.gamma"].data, p[b + "ln2.beta"].data, ws.v[j], ws.mr2[j],
                    M, El, E, m.eps)
         chan_fwd(m, g, ws.v[j], _panel(m, g, b + "ch1.w"), M, El, H, epi=E_BCOL | E_GF,
@@ -518,7 +541,7 @@ def backward_grid(m, ws) -> None:
         hx = g.row.dest((M, El), od, slot="gx2")                # g_x2 operand copy -> row group
         # (same pass: tok2's row-bias gradient partial = row sums of this rank's g_x2 columns)
         m._ln_bwd(ws.x2[j], ws.gv, b + "ln2.", ws.mr2[j], ws.bst2[j], gf, ws.gx2, hx.own, M, El, E,
-                  row_reduce=ctx.all_reduce_row, bcast=hx.peers, moments=False,
+                  row_reduce=lambda t: row_reduce(m, g, t), bcast=hx.peers, moments=False,
                   sums=dict(rowsum=p[b + "tok2.b"].grad, rowsum_period=Tl))
         g.row.publish(hx)
         xall = hx.planes.view(m.C, B, Tl, El)
@@ -532,7 +555,7 @@ def backward_grid(m, ws) -> None:
         # (same pass: column sums of g = the bias gradient of the previous block's ch2 / the encoder)
         nxt = f"block{(j - 1) % cfg.n_blocks}.ch2.b" if j > 0 else "enc.b"
         m._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, gf, hg.own, M, El, E,
-                  row_reduce=ctx.all_reduce_row, bcast=hg.peers, sums=dict(colsum=p[nxt].grad))
+                  row_reduce=lambda t: row_reduce(m, g, t), bcast=hg.peers, sums=dict(colsum=p[nxt].grad))
         g.row.publish(hg)
     chan_bwd(m, g, None, ws.xp, _panel(m, g, "enc.w"), M, Fl, E, "enc.w", "enc.b", None, dyrow=hg.planes)
 
@@ -596,7 +619,10 @@ def step_exchange_bytes(m, batch: int, r: int = 1, op_bytes: int | None = None, 
     # group, the loss over the grid, duplicated-vector gradients over their sharing groups
     ar = 0.0
     ring = lambda G, nbytes: 2.0 * (G - 1) / G * nbytes  # noqa: E731
-    if C > 1:
+    gw = getattr(getattr(m, "_ws", None), "grid", None)
+    if C > 1 and gw is not None and gw.peer_moments:
+        ex += 4 * nj * (C - 1) * M * 2 * 4  # pushed to the row group's moment slots
+    elif C > 1:
         ar += 4 * nj * ring(C, M * 2 * 4)
     ar += ring(m.ctx.n, 4)
     f = m.flat
