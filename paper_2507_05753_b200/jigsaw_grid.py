@@ -464,6 +464,116 @@ def tok1_bwd_all(m, g, ws, j, b, ghcols):
         K.gemm(out, urow, ghcols[bi], KM, MN, Tl, Kl, El, C, B * Tl * El, El * Kl, reduce_batch=True, **kw)
 
 
+# ------------------------------------- token layers, B > 1: plane-major, batched over samples
+# For B > 1 the token-mixing tensors of the grid step are kept PLANE-MAJOR: chunk j (El rows of
+# the E axis) of every sample next to each other, [C][B][El][Kl] — the gathered u and g_x2 (row
+# group slots, [C][B][Tl][El]), the tok1 output h / gelu(h) and the gradient gh (at R = 1 the
+# local buffers reinterpreted; at R > 1 the column-group gather slots, filled through dest_pm).
+# Then every per-(chunk, sample) product has ONE uniform stride, so the local token GEMMs (tok1
+# forward and the gh GEMM at R = 1) and both weight-gradient GEMMs (dW1, dW2: a reduction over
+# chunks AND samples) are one launch per layer instead of one per sample; the reduce-scatter
+# GEMMs stay per sample (their owner planes are per sample) and run side by side (g.fan).
+def _pm_path(m, g, ws) -> bool:
+    return ws.B > 1 and not g.fused
+
+
+def _pm_view(t: torch.Tensor, C: int, B: int, El: int, Kl: int) -> torch.Tensor:
+    return t.reshape(-1)[:C * B * El * Kl].view(C, B, El, Kl)
+
+
+def tok1_fwd_pm(m, g, ws, j, b, uall):
+    """h = u^T W1 + b1, a = gelu(h) for all samples; uall [C, B, Tl, El] (row-gathered u).
+    Returns a plane-major [C, B, El, Kl] (tok2's operand, dW2's B operand)."""
+    p, R, C, B = m.params, m.R, m.C, ws.B
+    Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
+    if R == 1:
+        hv, av = _pm_view(ws.h[j], C, B, El, Kl), _pm_view(ws.a[j], C, B, El, Kl)
+        K.gemm(hv, uall, p[b + "tok1.w"].op, MN, MN, El, Kl, Tl, C * B, Tl * El, 0, d_bs=El * Kl,
+               epi=E_BCOL | E_GF, bias=p[b + "tok1.b"].data, d2=av, d2_bs=El * Kl)
+        return av
+    q, ps = g.q, B * Tl * El
+    fns, has = [], []
+    for bi in range(B):
+        urow = uall[:, bi]
+
+        def fn(s, D, d_bs, dpl, urow=urow, **kw):
+            K.gemm(D, urow[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
+                   d_planes=dpl, lda=El, **kw)
+        fns.append(fn)
+        has.append(g.col.dest_pm((Er, Kl), m.op_dtype, f"a_col{j}", bi, B, q))
+    res = g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q, run=g.fan)
+    g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Er, Kl, acc_bs=r[2], nplanes=r[1], epi=E_BCOL | E_GF,
+                                         bias=p[b + "tok1.b"].data, d=ws.h[j][bi], d2=has[bi].own,
+                                         d2_bcast=has[bi].peers) for bi, r in enumerate(res)])
+    g.col.publish_all(has)
+    return _pm_view(g.col.persistent(f"a_col{j}"), C, B, El, Kl)
+
+
+def tok2_fwd_pm(m, g, ws, j, b, av):
+    """x2 = x + W2 a^T + b2[:, None] per sample (RS over the row group), side by side."""
+    p, C, B = m.params, m.C, ws.B
+    Tl, El, Kl = ws.Tl, ws.El, ws.Kl
+    fns = []
+    for bi in range(B):
+        def fn(s, D, d_bs, dpl, a0=av[0, bi], **kw):
+            K.gemm(D, p[b + "tok2.w"].op, a0, KM, KM, Tl, El, Kl, C, 0, B * El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
+        fns.append(fn)
+    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, run=g.fan)
+    g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Tl, El, acc_bs=r[2], nplanes=r[1], epi=E_BROW | E_RES | E_ST,
+                                         bias=p[b + "tok2.b"].data, resid=ws.res[j][bi], d=ws.x2[j][bi],
+                                         stats=ws.st2[j][bi * Tl:(bi + 1) * Tl]) for bi, r in enumerate(res)])
+
+
+def tok2_bwd_pm(m, g, ws, j, b, xall, av):
+    """gh = (g_x2^T W2) * gelu'(h) for all samples (plane-major), the tok1 bias gradient, and
+    dW2 = sum over chunks and samples of g_x2 a — one GEMM. xall [C, B, Tl, El]."""
+    p, R, C, B = m.params, m.R, m.C, ws.B
+    Tl, El, Er, Kl = ws.Tl, ws.El, ws.Er, ws.Kl
+    if R == 1:
+        ghv = _pm_view(ws.gh, C, B, El, Kl)
+        K.gemm(ghv, xall, p[b + "tok2.w"].op, MN, MN, El, Kl, Tl, C * B, Tl * El, 0, d_bs=El * Kl, epi=E_GB,
+               pre=_pm_view(ws.h[j], C, B, El, Kl), p_bs=El * Kl)
+        K.colsum(ghv, p[b + "tok1.b"].grad, C * B * El, Kl)
+    else:
+        q, ps = g.q, B * Tl * El
+        fns, hgs = [], []
+        for bi in range(B):
+            grow = xall[:, bi]
+
+            def fn(s, D, d_bs, dpl, grow=grow, **kw):
+                K.gemm(D, grow[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C, ps, 0, d_bs=d_bs,
+                       d_planes=dpl, lda=El, **kw)
+            fns.append(fn)
+            hgs.append(g.col.dest_pm((Er, Kl), m.op_dtype, "gh_col", bi, B, q))
+        res = g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q, run=g.fan)
+        g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Er, Kl, acc_bs=r[2], nplanes=r[1], epi=E_GB, pre=ws.h[j][bi],
+                                             d=hgs[bi].own, d_bcast=hgs[bi].peers) for bi, r in enumerate(res)])
+        for hg in hgs:  # (into one bias gradient: in order)
+            K.colsum(hg.own, p[b + "tok1.b"].grad, Er, Kl)
+        g.col.publish_all(hgs)
+        ghv = _pm_view(g.col.persistent("gh_col"), C, B, El, Kl)
+    out, kw = m._wgrad(b + "tok2.w")
+    K.gemm(out, xall, av, KM, MN, Tl, Kl, El, C * B, Tl * El, El * Kl, reduce_batch=True, **kw)
+    return ghv
+
+
+def tok1_bwd_pm(m, g, ws, j, b, uall, ghv):
+    """gu = W1 gh^T per sample (RS over the row group, side by side); dW1 = sum over chunks and
+    samples of u gh — one GEMM."""
+    p, C, B = m.params, m.C, ws.B
+    Tl, El, Kl = ws.Tl, ws.El, ws.Kl
+    fns = []
+    for bi in range(B):
+        def fn(s, D, d_bs, dpl, g0=ghv[0, bi], **kw):
+            K.gemm(D, p[b + "tok1.w"].op, g0, KM, KM, Tl, El, Kl, C, 0, B * El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
+        fns.append(fn)
+    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, outs=[ws.gu[bi] for bi in range(B)], run=g.fan)
+    g.fan([lambda bi=bi, r=r: K.sum_planes(ws.gu[bi], r[0], Tl * El, r[1], r[2]) for bi, r in enumerate(res)
+           if r[1] > 1 or r[0].data_ptr() != ws.gu[bi].data_ptr()])
+    out, kw = m._wgrad(b + "tok1.w")
+    K.gemm(out, uall, ghv, KM, MN, Tl, Kl, El, C * B, Tl * El, El * Kl, reduce_batch=True, **kw)
+
+
 # --------------------------------------------------------------------------- forward / backward
 def forward_grid(m, ws) -> None:
     g = _gw(m, ws)
@@ -492,8 +602,11 @@ def forward_grid(m, ws) -> None:
                    M, El, E, m.eps, bcast=hu.peers)
         g.row.publish(hu)
         uall = hu.planes.view(C, B, Tl, El)
-        acols = tok1_fwd_all(m, g, ws, j, b, uall)
-        tok2_fwd_all(m, g, ws, j, b, acols)
+        if _pm_path(m, g, ws):
+            tok2_fwd_pm(m, g, ws, j, b, tok1_fwd_pm(m, g, ws, j, b, uall))
+        else:
+            acols = tok1_fwd_all(m, g, ws, j, b, uall)
+            tok2_fwd_all(m, g, ws, j, b, acols)
         row_reduce(m, g, ws.st2[j])
         K.ln_apply(ws.x2[j], ws.st2[j], p[b + "ln2.gamma"].data, p[b + "ln2.beta"].data, ws.v[j], ws.mr2[j],
                    M, El, E, m.eps)
@@ -545,12 +658,17 @@ def backward_grid(m, ws) -> None:
                   sums=dict(rowsum=p[b + "tok2.b"].grad, rowsum_period=Tl))
         g.row.publish(hx)
         xall = hx.planes.view(m.C, B, Tl, El)
-        acol_all = g.col.persistent(f"a_col{j}").view(B, -1, Kl) if m.R > 1 else None
-        acols = [acol_all[bi] if m.R > 1 else ws.a[j][bi] for bi in range(B)]
-        ghs = tok2_bwd_all(m, g, ws, j, b, xall, acols)
-        for gh_local, _ in ghs:
-            K.colsum(gh_local, p[b + "tok1.b"].grad, Er, Kl)
-        tok1_bwd_all(m, g, ws, j, b, [ghcol for _, ghcol in ghs])
+        if _pm_path(m, g, ws):
+            av = _pm_view(g.col.persistent(f"a_col{j}") if m.R > 1 else ws.a[j], m.C, B, El, Kl)
+            ghv = tok2_bwd_pm(m, g, ws, j, b, xall, av)
+            tok1_bwd_pm(m, g, ws, j, b, g.row.persistent(f"u_row{j}").view(m.C, B, Tl, El), ghv)
+        else:
+            acol_all = g.col.persistent(f"a_col{j}").view(B, -1, Kl) if m.R > 1 else None
+            acols = [acol_all[bi] if m.R > 1 else ws.a[j][bi] for bi in range(B)]
+            ghs = tok2_bwd_all(m, g, ws, j, b, xall, acols)
+            for gh_local, _ in ghs:
+                K.colsum(gh_local, p[b + "tok1.b"].grad, Er, Kl)
+            tok1_bwd_all(m, g, ws, j, b, [ghcol for _, ghcol in ghs])
         hg = g.row.dest((M, El), od, slot="g")                  # g operand copy -> row group
         # (same pass: column sums of g = the bias gradient of the previous block's ch2 / the encoder)
         nxt = f"block{(j - 1) % cfg.n_blocks}.ch2.b" if j > 0 else "enc.b"

@@ -38,8 +38,17 @@ class Gather:
     memory) also stores it at every address in `peers`; after publish(), `planes` [G, *shape]
     holds every member's block."""
 
-    def __init__(self, planes, own, peers):
+    def __init__(self, planes, own, peers, pm=None):
         self.planes, self.own, self.peers = planes, own, peers
+        self.pm = pm  # plane-major destination (slot tensor, sub, nsub, q) of dest_pm, NCCL publish
+
+
+def pm_block(r: int, sub: int, nsub: int, q: int) -> int:
+    """Block index of member r's sample `sub` in a plane-major gather slot [G/q][nsub][q][block]:
+    members r = j*q .. j*q+q-1 (one chunk j of the gathered rows) of every sample next to each
+    other, chunk-major over the samples — so chunk j of sample b sits at (j*nsub + b) * q blocks,
+    one uniform stride for a GEMM batched over (chunk, sample)."""
+    return ((r // q) * nsub + sub) * q + r % q
 
 
 class NcclTransport:
@@ -89,8 +98,27 @@ class NcclTransport:
         planes = self._slot(slot, nsub * self.G * n, dtype).view(nsub, self.G, *shape)[sub]
         return Gather(planes, self._buf(("own", slot, sub), n, dtype).view(*shape), [])
 
+    def dest_pm(self, shape, dtype, slot: str, sub: int, nsub: int, q: int) -> Gather:
+        """Gather destination whose members' blocks land plane-major in `slot` (see pm_block)."""
+        n = 1
+        for s_ in shape:
+            n *= s_
+        return Gather(None, self._buf(("own", slot, sub), n, dtype).view(*shape), [],
+                      pm=(self._persist[slot], sub, nsub, q))
+
     def publish(self, h: Gather) -> None:
         self.bytes_sent += (self.G - 1) * h.own.numel() * h.own.element_size()
+        if h.pm is not None:
+            slot, sub, nsub, q = h.pm
+            tmp = self._buf(("pm", h.own.numel()), self.G * h.own.numel(), h.own.dtype)
+            if self.G == 1:
+                tmp.copy_(h.own.reshape(-1))
+            else:
+                dist.all_gather_into_tensor(tmp, h.own.reshape(-1), group=self.group)
+            n = h.own.numel()
+            dst = slot.view(-1)[:self.G * nsub * n].view(self.G // q, nsub, q * n)[:, sub]
+            dst.copy_(tmp.view(self.G // q, q * n))  # (NCCL path: the scatter into the plane-major slot)
+            return
         if self.G == 1:
             h.planes[0].copy_(h.own)
         else:
@@ -267,6 +295,20 @@ class SymmTransport:
         planes = self._view(off, (self.G, *shape), dtype)
         peers = [self.base[j] + off + self.idx * nbytes for j in range(self.G) if j != self.idx]
         return Gather(planes, planes[self.idx], peers)
+
+    def dest_pm(self, shape, dtype, slot: str, sub: int, nsub: int, q: int) -> Gather:
+        """Gather destination whose members' blocks land plane-major in `slot` (see pm_block):
+        the producer stores its block at the same position of every member's slot."""
+        n = 1
+        for s_ in shape:
+            n *= s_
+        nbytes = n * torch.empty((), dtype=dtype).element_size()
+        blk = pm_block(self.idx, sub, nsub, q)
+        off = self._slot_off(slot, 0, nsub * nbytes)  # (capacity check for G x nsub blocks)
+        pos = off + blk * nbytes
+        own = self._view(pos, shape, dtype)
+        peers = [self.base[j] + pos for j in range(self.G) if j != self.idx]
+        return Gather(None, own, peers, pm=(self.persistent(slot), sub, nsub, q))
 
     def publish(self, h: Gather) -> None:
         self.bytes_sent += len(h.peers) * h.own.numel() * h.own.element_size()
