@@ -65,7 +65,9 @@ def summarize_launches(tag, path):
         bw = (a["rd"] + a["wr"]) / a["ns"] if a["ns"] else 0.0
         out.append(f"| {k} | {a['n']} | {a['ns'] / 1e6:.3f} | {100 * a['ns'] / tot:.1f}% | "
                    f"{a['tc'] / a['ns'] if a['ns'] else 0:.1f}% | {bw:.0f} |")
-    with open(os.path.join(ROOT, "profiles", f"{tag}_launches.csv"), "w", newline="") as f:
+    outdir = os.environ.get("NCU_SUMMARY_OUT", os.path.join(ROOT, "profiles"))
+    os.makedirs(outdir, exist_ok=True)
+    with open(os.path.join(outdir, f"{tag}_launches.csv"), "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "launches", "total_ns", "share", "dram_read_bytes", "dram_write_bytes", "tensor_active_pct"])
         for k, a in rows:
@@ -119,11 +121,13 @@ def main():
     out, traffic = summarize_launches(a.tag, lp)
     if os.path.exists(fp):
         out += summarize_full(fp)
-    md = os.path.join(ROOT, "profiles", f"{a.tag}_launches.md")
+    outdir = os.environ.get("NCU_SUMMARY_OUT", os.path.join(ROOT, "profiles"))
+    os.makedirs(outdir, exist_ok=True)
+    md = os.path.join(outdir, f"{a.tag}_launches.md")
     open(md, "w").write("\n".join(out) + "\n")
     json.dump({"tag": a.tag, "kernel": "gemm_kernel (all launches of one step)",
                "traffic_bytes_per_launch": traffic, "source": os.path.basename(lp)},
-              open(os.path.join(ROOT, "profiles", f"{a.tag}_gemm_traffic.json"), "w"), indent=1)
+              open(os.path.join(outdir, f"{a.tag}_gemm_traffic.json"), "w"), indent=1)
     print("\n".join(out))
 
 
