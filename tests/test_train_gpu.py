@@ -154,23 +154,23 @@ def test_scheduled_clipped_graph_steps_vs_oracle(cuda):
 
 def test_trainer_rollout_graphs_and_checkpoint_resume(cuda, tmp_path):
     """Trainer with r ~ U{1, 2} (one captured graph per r, shared Adam counter) on tiles from the
-    loader; a checkpoint taken mid-run and resumed reproduces the uninterrupted losses exactly."""
-    from paper_2507_05753_b200 import checkpoint as ck
+    loader; a run checkpointed mid-epoch (Trainer.save_checkpoint: weights, Adam state, epoch,
+    position, rollout-RNG state) and resumed by a fresh Trainer reproduces the uninterrupted run."""
     from paper_2507_05753_b200.data import TileLoader
     from paper_2507_05753_b200.engine import Trainer
     src = np.random.default_rng(9).standard_normal((8, 32, 64, 8)).astype(np.float32)
     m1 = _model("bf16")
     ld = TileLoader(src, m1.cfg, m1.ctx, lead=2, seed=1)
-    t1 = Trainer(m1, r_max=2, seed=4)
-    a = t1.train_epoch(ld, 0, max_steps=3)
-    assert int(t1.step_count.item()) >= 3 and len(t1.steps) >= 1
-    ck.save(t1.step_for(1), str(tmp_path))
-    b = t1.train_epoch(ld, 1, max_steps=3)
-    m2 = _model("bf16")
-    t2 = Trainer(m2, r_max=2, seed=4)
-    t2.draw_rollouts(3)  # same generator position as t1 after its first epoch
-    ck.load(t2.step_for(1), str(tmp_path))
-    c = t2.train_epoch(ld, 1, max_steps=3)
-    assert b["rollouts"] == c["rollouts"]
-    assert np.allclose(b["losses"], c["losses"], rtol=1e-5), (b, c)  # LN-moment atomics: order may differ
-    assert all(np.isfinite(a["losses"]))
+    full = Trainer(m1, r_max=2, seed=4).train_epoch(ld, 0)          # 6 steps, uninterrupted
+    t2 = Trainer(_model("bf16"), r_max=2, seed=4)
+    a = t2.train_epoch(ld, 0, max_steps=3)
+    assert int(t2.step_count.item()) == 3 and len(t2.steps) >= 1
+    t2.save_checkpoint(str(tmp_path))
+    t3 = Trainer(_model("bf16"), r_max=2, seed=123)
+    epoch, start = t3.load_checkpoint(str(tmp_path))
+    assert (epoch, start) == (0, 3)
+    c = t3.train_epoch(ld, epoch, start=start)
+    assert a["rollouts"] + c["rollouts"] == full["rollouts"]
+    # (LN-moment atomics: the summation order may differ run to run)
+    assert np.allclose(a["losses"] + c["losses"], full["losses"], rtol=1e-5), (a, c, full)
+    assert all(np.isfinite(full["losses"]))

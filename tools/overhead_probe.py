@@ -18,14 +18,16 @@ ctx = MpContext(comm, list(range(comm.world_size)))
 cfg_kw, lat_real, vars_real, _ = bench.CONFIGS[os.environ.get("CFG", "C4")]
 model = WeatherMixerModel(ctx, ModelConfig(**cfg_kw), init="fast", lat_real=lat_real, vars_real=vars_real)
 noop = lambda *a, **k: None  # noqa: E731
+from paper_2507_05753_b200 import jigsaw_grid as JG
 orig = {"barrier": TR.SymmTransport.barrier, "ar_row": MpContext.all_reduce_row, "ar_col": MpContext.all_reduce_col,
-        "copy": K.copy_async, "epilogue": K.epilogue}
+        "copy": K.copy_async, "epilogue": K.epilogue, "moments": JG.row_reduce}
 
 
 def restore():
     TR.SymmTransport.barrier = orig["barrier"]
     MpContext.all_reduce_row, MpContext.all_reduce_col = orig["ar_row"], orig["ar_col"]
     K.copy_async, K.epilogue = orig["copy"], orig["epilogue"]
+    JG.row_reduce = orig["moments"]
 
 
 def apply(v):
@@ -37,6 +39,8 @@ def apply(v):
         K.copy_async = noop
     if v == "noepilogue":
         K.epilogue = noop
+    if v in ("nomoments", "nocomm"):
+        JG.row_reduce = noop
 
 
 def timed(step, n=10):
@@ -55,7 +59,7 @@ def timed(step, n=10):
     return t.item()
 
 
-variants = sys.argv[1:] or ["base", "nobarrier", "noar", "nocopy", "noepilogue", "nocomm"]
+variants = sys.argv[1:] or ["base", "nobarrier", "noar", "nomoments", "nocopy", "noepilogue", "nocomm"]
 for v in variants:
     apply(v)
     step = TrainStep(model, batch=int(os.environ.get("B", "1")))
