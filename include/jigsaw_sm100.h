@@ -166,6 +166,11 @@ int jg_sum_planes(float* y, const void* x, int32_t x_type, int64_t n, int32_t np
 
 /* Asynchronous device copy (copy engine; either side may be a peer GPU's buffer over NVLink).
  * Used to push Jigsaw activation tiles into peers' symmetric gather buffers. */
+/* SM-driven copy of `bytes` (multiple of 8; src / dst 8-byte aligned) from src to every dst->ptr[i] (own or NVLink peer
+ * memory), ending with a system-scope fence: the small Jigsaw gathers (layer-norm row moments,
+ * model.py:220-231 stats_peer) that must not wait behind host->device copies on the copy
+ * engines. */
+int jg_push(const void* src, int64_t bytes, const jg_bcast* dst, void* stream);
 int jg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
 /* Device-side barrier of a Jigsaw group over peer memory (graph-capturable; publishes the

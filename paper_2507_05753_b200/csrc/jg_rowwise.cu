@@ -943,6 +943,27 @@ __global__ void axpy_kernel(float* __restrict__ y, const float* __restrict__ x, 
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// SM-driven copy of one buffer to up to 4 destinations (own or NVLink-mapped peer memory):
+// 16-byte vector loads / stores when everything is 16-byte aligned, else 8-byte. For the small
+// Jigsaw gathers (layer-norm row moments) that must not queue behind bulk host->device copies on
+// the copy engines.
+template <typename V>
+__global__ void push_kernel(const uint8_t* __restrict__ src, int64_t bytes, Bcast dst) {
+  const int64_t n = bytes / (int64_t)sizeof(V);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const V v = reinterpret_cast<const V*>(src)[i];
+    for (int d = 0; d < dst.n; ++d) reinterpret_cast<V*>(dst.p[d])[i] = v;
+  }
+  const int64_t t0 = n * (int64_t)sizeof(V);
+  if (blockIdx.x == 0 && (int64_t)threadIdx.x < (bytes - t0) / 8) {
+    const int64_t o = t0 + threadIdx.x * 8;
+    const uint2 v = *reinterpret_cast<const uint2*>(src + o);
+    for (int d = 0; d < dst.n; ++d) *reinterpret_cast<uint2*>(static_cast<uint8_t*>(dst.p[d]) + o) = v;
+  }
+  __threadfence_system();  // peers read after the group barrier that follows
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1294,6 +1315,25 @@ int jg_group_barrier(uint32_t* const* peer_slots, uint32_t* own_slots, uint32_t*
   a.idx = idx;
   group_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a);
   JG_LAUNCH_CHECK("group_barrier");
+  return JG_OK;
+}
+
+int jg_push(const void* src, int64_t bytes, const jg_bcast* dst, void* stream) {
+  auto al8 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; };
+  JG_SHAPE_CHECK(bytes >= 0 && bytes % 8 == 0 && al8(src), "jg_push: bytes and src must be 8-byte multiples");
+  Bcast b = to_bcast(dst);
+  bool a16 = al16(src);
+  for (int d = 0; d < b.n; ++d) {
+    JG_SHAPE_CHECK(al8(b.p[d]), "jg_push: destinations must be 8-byte aligned");
+    a16 = a16 && al16(b.p[d]);
+  }
+  if (bytes == 0 || b.n == 0) return JG_OK;
+  const uint8_t* s = static_cast<const uint8_t*>(src);
+  if (a16)
+    push_kernel<uint4><<<grid_for((bytes + 15) / 16, 256), 256, 0, (cudaStream_t)stream>>>(s, bytes, b);
+  else
+    push_kernel<uint2><<<grid_for((bytes + 7) / 8, 256), 256, 0, (cudaStream_t)stream>>>(s, bytes, b);
+  JG_LAUNCH_CHECK("push");
   return JG_OK;
 }
 

@@ -63,6 +63,12 @@ def copy_async(dst_ptr: int, src: torch.Tensor, nbytes: int | None = None):
     _lib.call("jg_copy_async", dst_ptr, src.data_ptr(), nbytes if nbytes is not None else src.numel() * src.element_size())
 
 
+def push(src: torch.Tensor, addrs, nbytes: int | None = None):
+    """SM-driven copy of `src` to up to 4 raw device addresses (own / NVLink peer memory)."""
+    _lib.call("jg_push", src.data_ptr(), nbytes if nbytes is not None else src.numel() * src.element_size(),
+              _bref(addrs))
+
+
 def axpy(y, x, alpha=1.0):
     _lib.call("jg_axpy", y.data_ptr(), x.data_ptr(), float(alpha), x.numel())
 

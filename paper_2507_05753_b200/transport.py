@@ -163,6 +163,7 @@ class NcclTransport:
 
 
 FLAG_CAP = 1 << 15  # arrival counters per reduce-scatter region (jg_gemm_desc.rs_flag_cap)
+PUSH_SM_BYTES = 4 << 20  # gathers up to this size are pushed by an SM kernel (jg_push), larger by copy engines
 
 
 def _run_all(calls) -> None:
@@ -280,8 +281,14 @@ class SymmTransport:
         nbytes = x.numel() * x.element_size()
         off = self._slot_off(slot, sub, nbytes)
         x = x.contiguous()
-        for j in range(self.G):  # push my block into slot idx of every member (copy engine)
-            K.copy_async(self.base[j] + off + self.idx * nbytes, x, nbytes)
+        dsts = [self.base[j] + off + self.idx * nbytes for j in range(self.G)]
+        if nbytes <= PUSH_SM_BYTES and self.G <= 4 and nbytes % 8 == 0 and x.data_ptr() % 8 == 0 and off % 8 == 0:
+            # small gathers (layer-norm moments): stores from the SMs, so they never queue behind a
+            # bulk host->device copy on the copy engines (the e2e input feed)
+            K.push(x, dsts, nbytes)
+        else:
+            for d in dsts:  # push my block into slot idx of every member (copy engine)
+                K.copy_async(d, x, nbytes)
         self.bytes_sent += (self.G - 1) * nbytes
         self.barrier()
         return self._view(off, (self.G, *x.shape), x.dtype)

@@ -130,3 +130,24 @@ def test_gemm_and_rowwise_deterministic(cuda):
         ys.append(y)
     torch.cuda.synchronize()
     assert all(torch.equal(y, ys[0]) for y in ys[1:])
+
+
+@pytest.mark.parametrize("nbytes,off8", [(65520, 0), (32760, 1), (8, 0), (4 << 20, 0)])
+def test_push_copies_exactly(cuda, nbytes, off8):
+    """jg_push (SM-driven copy to up to 4 destinations, the layer-norm moment gathers): exact
+    copies, 16-byte or 8-byte aligned, nothing written outside the destinations."""
+    from paper_2507_05753_b200 import kernels as K
+    n = nbytes // 8
+    src = torch.randn(n + 1, dtype=torch.float64, device=cuda)[off8:off8 + n]
+    bufs, dsts = [], []
+    for d in range(3):
+        buf, view = _guarded(1, n + 1, n + 1, torch.float64)
+        dst = view.reshape(-1)[off8:off8 + n]
+        bufs.append((buf, dst))
+        dsts.append(dst.data_ptr())
+    K.push(src, dsts, nbytes)
+    torch.cuda.synchronize()
+    for buf, dst in bufs:
+        assert torch.equal(dst, src)
+        outside = torch.cat([buf[:4096 + off8], buf[4096 + off8 + n:]])
+        assert bool((outside == SENT).all())
