@@ -277,8 +277,10 @@ class TrainStep:
             cs = self._streams()
             if self._staged is not None and self._staged[0] is x and self._staged[1] is target:
                 cur.wait_event(self._stage_ev)
-                self.ws.xin.copy_(self._stage[0], non_blocking=True)
-                self.target.copy_(self._stage[1], non_blocking=True)
+                # staged inputs into place with an SM copy (jg_push), not a copy-engine memcpy that
+                # would queue behind the next step's host->device prefetch on the copy engines
+                K.push(self._stage[0], [self.ws.xin.data_ptr()])
+                K.push(self._stage[1], [self.target.data_ptr()])
                 self._staged = None
             else:
                 cs.wait_stream(cur)  # the previous step's loss half has finished reading the target
