@@ -141,6 +141,9 @@ typedef struct jg_gemm_desc {
    * stats_bstride); the moments go to `stats` (zeroed by the caller). */
   const float* lnb_x; int64_t lnb_ldx, lnb_x_bstride;
   const float* lnb_gamma; const float* lnb_mr;
+  /* persistent grid limit: at most max_sms SMs (0 = all), leaving the rest to a concurrent
+   * kernel (the optimiser overlapped with the backward, jg_adam_sms) */
+  int32_t max_sms;
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);
@@ -266,6 +269,12 @@ int jg_blend_loss(const float* dec_tok, const float* x, const float* target, con
 int jg_adam(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n,
             float lr, float beta1, float beta2, float eps, const int32_t* step_dev,
             const float* grad_scale_dev, const float* lr_dev, void* stream);   /* lr_dev != NULL overrides lr */
+/* jg_adam pinned to `sms` SMs (one 1024-thread block per SM, holding enough shared memory that
+ * no GEMM CTA fits beside it): runs beside a persistent jg_gemm limited to the other SMs
+ * (jg_gemm_desc.max_sms), so a block's optimiser update overlaps the rest of the backward. */
+int jg_adam_sms(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n,
+                float lr, float beta1, float beta2, float eps, const int32_t* step_dev,
+                const float* grad_scale_dev, const float* lr_dev, int32_t sms, void* stream);
 /* jg_adam + Jigsaw weight-panel push: segment k of this call's range ([start, start+len),
  * 64-element aligned, len % 4 == 0) is additionally stored as bf16 at every dst[k][0..ndst)
  * (8-byte aligned) — the column-group members' gather slots of a channel-mixing weight, so the

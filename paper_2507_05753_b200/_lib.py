@@ -34,7 +34,7 @@ EXPORTED = [
     "jg_gemm", "jg_split_tf32", "jg_split_tf32_2d", "jg_cast_bf16", "jg_gelu_fwd", "jg_gelu_bwd",
     "jg_ln_moments", "jg_ln_apply", "jg_ln_bwd_moments", "jg_ln_bwd_apply",
     "jg_colsum", "jg_rowsum", "jg_patchify", "jg_unpatchify", "jg_blend_loss",
-    "jg_adam", "jg_adam_push", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async", "jg_push",
+    "jg_adam", "jg_adam_sms", "jg_adam_push", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async", "jg_push",
     "jg_group_barrier", "jg_opt_schedule", "jg_version", "jg_last_error", "jg_launch_count",
 ]
 JG_MAX_LR_CLASSES = 4
@@ -43,6 +43,18 @@ JG_MAX_LR_CLASSES = 4
 class Bcast(ctypes.Structure):
     """jg_bcast: up to 4 extra destinations of an output (peer gather slots)."""
     _fields_ = [("ptr", ctypes.c_void_p * 4), ("n", ctypes.c_int32)]
+
+
+_NUM_SMS = None
+
+
+def num_sms() -> int:
+    """SM count of the current device (148 on B200)."""
+    global _NUM_SMS
+    if _NUM_SMS is None:
+        import torch
+        _NUM_SMS = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return _NUM_SMS
 
 
 def make_bcast(addrs) -> "Bcast | None":
@@ -119,6 +131,7 @@ class GemmDesc(ctypes.Structure):
         ("rs_own", ctypes.c_int32), ("rs_need", ctypes.c_int32), ("rs_flag_cap", ctypes.c_int32),
         ("lnb_x", ctypes.c_void_p), ("lnb_ldx", ctypes.c_int64), ("lnb_x_bstride", ctypes.c_int64),
         ("lnb_gamma", ctypes.c_void_p), ("lnb_mr", ctypes.c_void_p),
+        ("max_sms", ctypes.c_int32),
     ]
 
 
@@ -155,6 +168,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_unpatchify": [vp, vp, i64, i64, i64, i64, i64, i64, vp],
         "jg_blend_loss": [vp] * 12 + [i64] * 6 + [f32, f32, vp, vp],
         "jg_adam": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp, vp],
+        "jg_adam_sms": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp, i32, vp],
         "jg_adam_push": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, vp, vp, vp, ctypes.POINTER(PushTable), vp],
         "jg_step_increment": [vp, vp],
         "jg_sqnorm": [vp, i64, f32, vp, vp],

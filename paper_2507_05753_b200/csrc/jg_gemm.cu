@@ -973,8 +973,9 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   p.num_tiles = static_cast<int>(nt);
   p.num_pos = p.num_tiles;
   {
-    static const int sm_cap = getenv("JG_GEMM_SMS") ? atoi(getenv("JG_GEMM_SMS")) : 0;  // experiment only
-    const int sms = (sm_cap > 0 && sm_cap < jg::num_sms()) ? sm_cap : jg::num_sms();
+    static const int env_cap = getenv("JG_GEMM_SMS") ? atoi(getenv("JG_GEMM_SMS")) : 0;  // experiment only
+    const int sm_cap = g->max_sms > 0 ? g->max_sms : env_cap;
+    const int sms = (sm_cap >= 2 * cg && sm_cap < jg::num_sms()) ? sm_cap : jg::num_sms();
     const int max_units = sms / cg;
     p.units = p.num_tiles < max_units ? p.num_tiles : max_units;
   }

@@ -3,6 +3,7 @@
 // All are coalesced along the contiguous (last) axis, vectorised to 16-byte accesses where
 // the row length allows, warp-reduced, and grid-sized in multiples of the SM count.
 #include "jg_common.cuh"
+#include <mutex>
 #include <cstring>
 
 namespace {
@@ -1195,6 +1196,26 @@ int jg_adam_push(float* p, const float* g, float* m, float* v, void* p_bf16, int
   adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
       p, g, m, v, (__nv_bfloat16*)p_bf16, n, lr, beta1, beta2, eps, step_dev, grad_scale_dev, lr_dev, t);
   JG_LAUNCH_CHECK("adam");
+  return JG_OK;
+}
+
+int jg_adam_sms(float* p, const float* g, float* m, float* v, void* p_bf16, int64_t n, float lr, float beta1,
+                float beta2, float eps, const int32_t* step_dev, const float* grad_scale_dev, const float* lr_dev,
+                int32_t sms, void* stream) {
+  JG_SHAPE_CHECK(n >= 0 && step_dev && sms > 0, "jg_adam_sms: bad arguments");
+  JG_SHAPE_CHECK(al16(p) && al16(g) && al16(m) && al16(v) && (!p_bf16 || (reinterpret_cast<uintptr_t>(p_bf16) & 7u) == 0),
+                 "jg_adam: buffers must be 16B aligned");
+  if (n == 0) return JG_OK;
+  // one 1024-thread block per SM (48 registers per thread) holding 100 KB of (unused) dynamic
+  // shared memory, so none fits beside a GEMM CTA: the blocks land on the SMs the GEMM grid
+  // leaves free
+  constexpr int kSmem = 100 * 1024;
+  static std::once_flag once;
+  std::call_once(once, [] { cudaFuncSetAttribute(adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem); });
+  jg_push_table t{};
+  adam_kernel<<<sms, 1024, kSmem, (cudaStream_t)stream>>>(p, g, m, v, (__nv_bfloat16*)p_bf16, n, lr, beta1, beta2,
+                                                              eps, step_dev, grad_scale_dev, lr_dev, t);
+  JG_LAUNCH_CHECK("adam_sms");
   return JG_OK;
 }
 

@@ -19,6 +19,7 @@ import torch
 
 from . import _lib
 from . import kernels as K
+from . import tensor as T
 from .errors import ConfigError
 from .model import WeatherMixerModel
 from .train import AdamConfig
@@ -77,6 +78,19 @@ class TrainStep:
         self.push_panels = (model.ctx.n > 1 and model.R > 1 and not self.fused_adam
                             and os.environ.get("JIGSAW_PANEL_PUSH", "1") == "1")
         self._panel_version = None
+        # Adam overlapped with the backward (1 GPU): once block j's weight gradients are complete
+        # (the backward runs blocks last-to-first), its matrices' Adam runs on a side stream pinned
+        # to `adam_sms` SMs (jg_adam_sms) while the remaining backward GEMMs use the other SMs
+        # (jg_gemm_desc.max_sms); the first block, the encoder / decoder and the vectors are updated
+        # after the backward on every SM. Needs the whole step's gradient-free schedule: no
+        # clipping (global norm first), no dp_reduce, one gradient GEMM per weight (rollout 1).
+        self.adam_sms = int(os.environ.get("JIGSAW_ADAM_SMS", "16"))
+        self.adam_overlap = (os.environ.get("JIGSAW_ADAM_OVERLAP", "1") == "1" and self.adam_sms > 0
+                             and model.ctx.n == 1 and r == 1 and not self.fused_adam and self.clip is None
+                             and model.ctx.dp_replicas == 1 and model.device.type == "cuda"
+                             and model.cfg.n_blocks > 1)
+        self._early: list[tuple[int, int]] = []
+        self._adam_stream = None
 
     # -- the step body --------------------------------------------------------------------
     def _body(self) -> None:
@@ -109,21 +123,62 @@ class TrainStep:
             m.ctx.all_reduce_all(ws.loss)  # the loss is a sum of per-tile terms
         m._fused_adam = (self.step_count, self.adam) if self.fused_adam and not self._dry else None
         m._grad_overwrite = self.overwrite
+        overlap = self.adam_overlap and not self._dry
+        self._early = []
+        if overlap:
+            if self.scheduled:  # this step's lr (no clipping here: it needs no gradient)
+                K.opt_schedule(self.step_count, [self.adam.schedule(c) for c in m.flat.CLASSES], self.sqsum, None,
+                               self.lr_dev, self.grad_scale)
+            m._after_block_bwd = self._early_adam
         try:
             m._backward(ws)
         finally:
             m._fused_adam = None
             m._grad_overwrite = False
+            m._after_block_bwd = None
+            T.GEMM_SM_CAP = 0
         m.grad_sync()
         m.ctx.all_reduce_dp_mean(m.flat.grad)  # dp_reduce over replicas of this shard (no-op for one)
         if self._dry:
             return
         if self.clip is not None:
             self._global_sqnorm()
-        if self.clip is not None or self.scheduled:
+        if (self.clip is not None or self.scheduled) and not overlap:
             K.opt_schedule(self.step_count, [self.adam.schedule(c) for c in m.flat.CLASSES], self.sqsum, self.clip,
                            self.lr_dev, self.grad_scale)
         self._adam()
+        if self._early:
+            torch.cuda.current_stream().wait_stream(self._adam_stream)  # join the early updates
+
+    def _block_range(self, j: int) -> tuple[int, int]:
+        """Flat range of block j's weight matrices (contiguous: lr class, then kind, then order)."""
+        f = self.model.flat
+        names = [f"block{j}.{w}" for w in ("tok1.w", "tok2.w", "ch1.w", "ch2.w")]
+        lo = min(f.offsets[n] for n in names)
+        hi = max(f.offsets[n] + f.params[n].data.numel() for n in names)
+        return lo, hi
+
+    def _early_adam(self, j: int) -> None:
+        """Backward hook after block j: its matrices' Adam on the side stream, pinned to adam_sms
+        SMs; the GEMMs issued from here on leave those SMs free. Block 0 (last in the backward)
+        waits for the full-GPU Adam after the backward."""
+        if j == 0:
+            return
+        m, f, a = self.model, self.model.flat, self.adam
+        if self._adam_stream is None:
+            self._adam_stream = torch.cuda.Stream(device=m.device)
+        lo, hi = self._block_range(j)
+        cls = "body"
+        ci = list(f.class_range).index(cls)
+        op_copy = f.op if f.op is not f.master else None
+        cur, side = torch.cuda.current_stream(), self._adam_stream
+        side.wait_stream(cur)  # block j's gradients are written
+        with torch.cuda.stream(side):
+            K.adam(f.master[lo:], f.grad[lo:], f.m[lo:], f.v[lo:], None if op_copy is None else op_copy[lo:], hi - lo,
+                   a.lr(cls), a.beta1, a.beta2, a.eps, self.step_count,
+                   lr_dev=self.lr_dev[ci:ci + 1] if self.scheduled else None, sms=self.adam_sms)
+        self._early.append((lo, hi))
+        T.GEMM_SM_CAP = _lib.num_sms() - self.adam_sms
 
     def _global_sqnorm(self) -> None:
         """Squared L2 norm of the global gradient: local shards summed over the
@@ -148,6 +203,18 @@ class TrainStep:
         from .jigsaw_grid import panel_push_segments
         f, a = self.model.flat, self.adam
         op_copy = f.op if f.op is not f.master else None
+        if self._early:
+            # the rest of every class after the early (overlapped) block updates
+            for i, (cls, (lo, hi)) in enumerate(f.class_range.items()):
+                cuts = sorted(r for r in self._early if lo <= r[0] < hi)
+                pos = lo
+                for a0, a1 in cuts + [(hi, hi)]:
+                    if a0 > pos:
+                        K.adam(f.master[pos:], f.grad[pos:], f.m[pos:], f.v[pos:],
+                               None if op_copy is None else op_copy[pos:], a0 - pos, a.lr(cls), a.beta1, a.beta2,
+                               a.eps, self.step_count, lr_dev=self.lr_dev[i:i + 1] if self.scheduled else None)
+                    pos = max(pos, a1)
+            return
         push = self._pushing()
         if push:
             # no column-group member may still be reading this step's panels (the encoder's dW

@@ -130,10 +130,16 @@ def blend_loss(dec, xin, target, blend_w, lat_w, var_w, g_ext, out, loss, g_blen
               batch, lat, lon, chans, pl, pw, float(inv_count), float(loss_scale), _bref(bcast))
 
 
-def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None, push=None):
+def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None, push=None, sms=None):
     """jg_adam; lr_dev (device float, e.g. one entry of the schedule's output) overrides lr.
     push: [(start, len, [addr, ...])] — ranges whose bf16 copy is also stored at peer addresses
-    (jg_adam_push: the Jigsaw weight-panel gather done by the optimiser)."""
+    (jg_adam_push: the Jigsaw weight-panel gather done by the optimiser). sms: pinned to that
+    many SMs (jg_adam_sms), beside a GEMM limited to the others."""
+    if sms:
+        assert not push, "jg_adam_sms has no panel push"
+        _lib.call("jg_adam_sms", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), ptr(p_op), n, float(lr),
+                  float(beta1), float(beta2), float(eps), step.data_ptr(), ptr(grad_scale), ptr(lr_dev), int(sms))
+        return
     if push:
         t = _lib.make_push_table(push)
         _lib.call("jg_adam_push", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), ptr(p_op), n, float(lr),

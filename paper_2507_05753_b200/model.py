@@ -565,6 +565,9 @@ class WeatherMixerModel:
             nxt = f"block{(j - 1) % cfg.n_blocks}.ch2.b" if j > 0 else "enc.b"
             self._ln_bwd(ws.res[j], ws.gu, b + "ln1.", ws.mr1[j], ws.bst1[j], ws.gx2, g, g_op, M, E, moments=False,
                          sums=dict(colsum=p[nxt].grad))
+            hook = getattr(self, "_after_block_bwd", None)
+            if hook is not None:  # block j's weight gradients are complete (TrainStep: early Adam)
+                hook(j)
         # encoder (NT): dWenc += g^T xp ; db += sum g (the input gradient is not needed, model.py:444-445)
         out, kw = self._wgrad("enc.w")
         self._gemm(out, g_op, ws.xp, MN, MN, E, F, M, **kw)

@@ -380,7 +380,7 @@ def opt_schedule(step, scheds, sqsum, clip_norm, lr_out, grad_scale):
         grad_scale.fill_(f)
 
 
-def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None, push=None):
+def adam(p, g, m, v, p_op, n, lr, beta1, beta2, eps, step, grad_scale=None, lr_dev=None, push=None, sms=None):
     t = int(step.item())
     if lr_dev is not None:
         lr = float(lr_dev.item())
