@@ -84,8 +84,10 @@ class TrainStep:
         # (jg_gemm_desc.max_sms); the first block, the encoder / decoder and the vectors are updated
         # after the backward on every SM. Needs the whole step's gradient-free schedule: no
         # clipping (global norm first), no dp_reduce, one gradient GEMM per weight (rollout 1).
+        # Measured NOT faster on C4 (power-capped: the GEMMs lose what Adam gains; 25.4-25.9 vs
+        # 25.9-26.0 samples/s with 16 / 24 SMs, 20 with 8), so it is an option, off by default.
         self.adam_sms = int(os.environ.get("JIGSAW_ADAM_SMS", "16"))
-        self.adam_overlap = (os.environ.get("JIGSAW_ADAM_OVERLAP", "1") == "1" and self.adam_sms > 0
+        self.adam_overlap = (os.environ.get("JIGSAW_ADAM_OVERLAP", "0") == "1" and self.adam_sms > 0
                              and model.ctx.n == 1 and r == 1 and not self.fused_adam and self.clip is None
                              and model.ctx.dp_replicas == 1 and model.device.type == "cuda"
                              and model.cfg.n_blocks > 1)
