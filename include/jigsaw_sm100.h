@@ -144,6 +144,12 @@ typedef struct jg_gemm_desc {
   /* persistent grid limit: at most max_sms SMs (0 = all), leaving the rest to a concurrent
    * kernel (the optimiser overlapped with the backward, jg_adam_sms) */
   int32_t max_sms;
+  /* d_planes with several samples per plane: with plane_div > 0, output batch b goes to plane
+   * b / plane_div (d_planes[b / plane_div], at most 8 planes), at sample offset
+   * (b % plane_div) * d_planes_bstride elements — one launch for the partial planes of every
+   * sample of a Jigsaw token layer (parallel.py:118-132 per sample). TMA-store epilogue only. */
+  int32_t plane_div;
+  int64_t d_planes_bstride;
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);

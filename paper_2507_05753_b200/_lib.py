@@ -132,6 +132,7 @@ class GemmDesc(ctypes.Structure):
         ("lnb_x", ctypes.c_void_p), ("lnb_ldx", ctypes.c_int64), ("lnb_x_bstride", ctypes.c_int64),
         ("lnb_gamma", ctypes.c_void_p), ("lnb_mr", ctypes.c_void_p),
         ("max_sms", ctypes.c_int32),
+        ("plane_div", ctypes.c_int32), ("d_planes_bstride", ctypes.c_int64),
     ]
 
 

@@ -68,6 +68,7 @@ struct GemmParams {
   void* d_planes[8];
   int remote;              // some output goes to a peer: system-scope fence at the end
   int planes;              // d_planes in use: per-batch D store maps
+  int plane_div;           // > 0: batch b -> store map b / plane_div, sample coordinate b % plane_div
   int plane_minor;         // tile order with the output plane fastest (JG_PLANE_MAJOR=1 disables)
   // fused reduce-scatter (jg_gemm_desc rs_*): raw partial tiles to the owners + arrival flags,
   // own-plane tiles last, summed with the peers' partials in this rank's buffer
@@ -694,9 +695,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             continue;
           }
           const bool per_batch_map = p.planes || (RS && p.rs_mode);
+          const int mi = per_batch_map ? (p.plane_div ? tb / p.plane_div : tb) : 0;
+          const int c2 = per_batch_map ? (p.plane_div ? tb % p.plane_div : 0) : tb;
           if (per_batch_map || p.d != nullptr)
-            stage_store(stg, v, p.dmap_bf16[per_batch_map ? tb : 0], lane, &p.tma_d[per_batch_map ? tb : 0], col0,
-                        rbase, per_batch_map ? 0 : tb, p.tma_dx, p.nb_d);
+            stage_store(stg, v, p.dmap_bf16[mi], lane, &p.tma_d[mi], col0, rbase, c2, p.tma_dx, p.nb_d);
           if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
             if (epi & JG_EPI_GELU_FWD) {
 #pragma unroll
@@ -1020,8 +1022,12 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
   p.rs_mode = rs_has_own ? 1 : 0;
   for (int i = 0; i < 8; ++i)
     if (g->rs_flag_peers[i] != nullptr) p.rs_mode = 1;
-  JG_SHAPE_CHECK(!p.remote || (!g->reduce_batch && g->batch <= 8 && !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM))),
-                 "jg_gemm: d_planes needs <= 8 independent output batches and no ACCUM/ADAM");
+  p.plane_div = (p.remote && g->plane_div > 0) ? g->plane_div : 0;
+  const int64_t nplanes_out = p.plane_div ? g->batch / p.plane_div : g->batch;
+  JG_SHAPE_CHECK(!p.plane_div || (g->batch % p.plane_div == 0 && !p.rs_mode && g->d_planes_bstride > 0),
+                 "jg_gemm: plane_div needs batch = planes x plane_div, a sample stride, no fused reduce-scatter");
+  JG_SHAPE_CHECK(!p.remote || (!g->reduce_batch && nplanes_out <= 8 && !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM))),
+                 "jg_gemm: d_planes needs <= 8 independent output planes and no ACCUM/ADAM");
   if (p.rs_mode) {
     JG_SHAPE_CHECK(!g->reduce_batch && g->batch <= 8 && p.rs_own >= -1 && p.rs_own < g->batch && !(epi & (JG_EPI_ACCUM | JG_EPI_ADAM)),
                    "jg_gemm: fused reduce-scatter needs <= 8 independent output batches and no ACCUM/ADAM");
@@ -1084,6 +1090,13 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
         const bool own = b == p.rs_own;
         p.dmap_bf16[b] = own ? dbf : p.rs_part_bf16;
         int rc = make_store_map(&p.tma_d[b], own ? g->d : g->d_planes[b], p.dmap_bf16[b], g->m, g->n, g->ldd, 0, 1);
+        if (rc) return rc;
+      }
+    } else if (p.remote && p.plane_div) {
+      for (int b = 0; b < static_cast<int>(nplanes_out); ++b) {
+        JG_SHAPE_CHECK(g->d_planes[b] != nullptr, "jg_gemm: plane_div needs every d_planes entry");
+        p.dmap_bf16[b] = dbf;
+        int rc = make_store_map(&p.tma_d[b], g->d_planes[b], dbf, g->m, g->n, g->ldd, g->d_planes_bstride, p.plane_div);
         if (rc) return rc;
       }
     } else if (p.remote) {

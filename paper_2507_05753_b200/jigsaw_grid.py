@@ -501,7 +501,11 @@ def tok1_fwd_pm(m, g, ws, j, b, uall):
                    d_planes=dpl, lda=El, **kw)
         fns.append(fn)
         has.append(g.col.dest_pm((Er, Kl), m.op_dtype, f"a_col{j}", bi, B, q))
-    res = g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q, run=g.fan)
+
+    def fnb(s, D, dpl, pdiv, pbs):  # every (plane, sample) item in one launch: plane-major uall
+        K.gemm(D, uall[..., s * Er:], p[b + "tok1.w"].op, MN, MN, Er, Kl, Tl, C * B, Tl * El, 0,
+               d_planes=dpl, plane_div=pdiv, planes_bs=pbs, lda=El)
+    res = g.col.rs_gemm_batched(Er, Kl, g.pdt, B, fns, fnb, q=q, run=g.fan)
     g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Er, Kl, acc_bs=r[2], nplanes=r[1], epi=E_BCOL | E_GF,
                                          bias=p[b + "tok1.b"].data, d=ws.h[j][bi], d2=has[bi].own,
                                          d2_bcast=has[bi].peers) for bi, r in enumerate(res)])
@@ -518,7 +522,11 @@ def tok2_fwd_pm(m, g, ws, j, b, av):
         def fn(s, D, d_bs, dpl, a0=av[0, bi], **kw):
             K.gemm(D, p[b + "tok2.w"].op, a0, KM, KM, Tl, El, Kl, C, 0, B * El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
         fns.append(fn)
-    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, run=g.fan)
+
+    def fnb(s, D, dpl, pdiv, pbs):  # every (plane, sample) item in one launch: plane-major a
+        K.gemm(D, p[b + "tok2.w"].op, av, KM, KM, Tl, El, Kl, C * B, 0, El * Kl, d_planes=dpl,
+               plane_div=pdiv, planes_bs=pbs)
+    res = g.row.rs_gemm_batched(Tl, El, g.pdt, B, fns, fnb, run=g.fan)
     g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Tl, El, acc_bs=r[2], nplanes=r[1], epi=E_BROW | E_RES | E_ST,
                                          bias=p[b + "tok2.b"].data, resid=ws.res[j][bi], d=ws.x2[j][bi],
                                          stats=ws.st2[j][bi * Tl:(bi + 1) * Tl]) for bi, r in enumerate(res)])
@@ -545,7 +553,11 @@ def tok2_bwd_pm(m, g, ws, j, b, xall, av):
                        d_planes=dpl, lda=El, **kw)
             fns.append(fn)
             hgs.append(g.col.dest_pm((Er, Kl), m.op_dtype, "gh_col", bi, B, q))
-        res = g.col.rs_gemm_multi(Er, Kl, g.pdt, fns, q=q, run=g.fan)
+
+        def fnb(s, D, dpl, pdiv, pbs):  # every (plane, sample) item in one launch: plane-major g_x2
+            K.gemm(D, xall[..., s * Er:], p[b + "tok2.w"].op, MN, MN, Er, Kl, Tl, C * B, Tl * El, 0,
+                   d_planes=dpl, plane_div=pdiv, planes_bs=pbs, lda=El)
+        res = g.col.rs_gemm_batched(Er, Kl, g.pdt, B, fns, fnb, q=q, run=g.fan)
         g.fan([lambda bi=bi, r=r: K.epilogue(r[0], Er, Kl, acc_bs=r[2], nplanes=r[1], epi=E_GB, pre=ws.h[j][bi],
                                              d=hgs[bi].own, d_bcast=hgs[bi].peers) for bi, r in enumerate(res)])
         for hg in hgs:  # (into one bias gradient: in order)
@@ -567,7 +579,11 @@ def tok1_bwd_pm(m, g, ws, j, b, uall, ghv):
         def fn(s, D, d_bs, dpl, g0=ghv[0, bi], **kw):
             K.gemm(D, p[b + "tok1.w"].op, g0, KM, KM, Tl, El, Kl, C, 0, B * El * Kl, d_bs=d_bs, d_planes=dpl, **kw)
         fns.append(fn)
-    res = g.row.rs_gemm_multi(Tl, El, g.pdt, fns, outs=[ws.gu[bi] for bi in range(B)], run=g.fan)
+
+    def fnb(s, D, dpl, pdiv, pbs):  # every (plane, sample) item in one launch: plane-major gh
+        K.gemm(D, p[b + "tok1.w"].op, ghv, KM, KM, Tl, El, Kl, C * B, 0, El * Kl, d_planes=dpl,
+               plane_div=pdiv, planes_bs=pbs)
+    res = g.row.rs_gemm_batched(Tl, El, g.pdt, B, fns, fnb, outs=[ws.gu[bi] for bi in range(B)], run=g.fan)
     g.fan([lambda bi=bi, r=r: K.sum_planes(ws.gu[bi], r[0], Tl * El, r[1], r[2]) for bi, r in enumerate(res)
            if r[1] > 1 or r[0].data_ptr() != ws.gu[bi].data_ptr()])
     out, kw = m._wgrad(b + "tok1.w")

@@ -97,7 +97,8 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
               stats_bs: int = 0, d_bs: int | None = None, d2_bs: int | None = None,
               lda: int | None = None, ldb: int | None = None, ldd: int | None = None,
               a_lo: torch.Tensor | None = None, b_lo: torch.Tensor | None = None, adam=None,
-              d_planes=None, d_bcast=None, d2_bcast=None, rs: dict | None = None, lnb=None) -> torch.Tensor:
+              d_planes=None, d_bcast=None, d2_bcast=None, rs: dict | None = None, lnb=None, plane_div: int = 0,
+              planes_bs: int = 0) -> torch.Tensor:
     """Low-level fused GEMM: out[b] (op)= sum_k A[b](m,k) B[b](n,k) with epilogue `epi`.
 
     A/B majors follow include/jigsaw_sm100.h. fp32 operands run 3xTF32: the hi/lo split is
@@ -150,6 +151,7 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
     if d_planes is not None:
         for i, addr in enumerate(d_planes):
             d.d_planes[i] = addr
+        d.plane_div, d.d_planes_bstride = plane_div, planes_bs  # (batch b -> plane b / plane_div, sample b % plane_div)
     if rs is not None:
         # fused reduce-scatter (jg_gemm_desc rs_*): flags / peer flag arrays / partial-plane source
         d.rs_flags = rs.get("flags")

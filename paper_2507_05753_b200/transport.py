@@ -157,6 +157,11 @@ class NcclTransport:
             res.append((red, 1, 0))
         return res
 
+    def rs_gemm_batched(self, rows: int, cols: int, dtype, nsamples: int, fns, fn_batched=None, q: int = 1,
+                        outs=None, run=None):
+        """(peer-memory transport: one launch for all samples) here: per-sample reduce-scatters."""
+        return self.rs_gemm_multi(rows, cols, dtype, fns, q=q, outs=outs, run=run)
+
     def publish_all(self, hs) -> None:
         for h in hs:
             self.publish(h)
@@ -356,6 +361,27 @@ class SymmTransport:
         (run or _run_all)(calls)
         self.barrier()
         return res
+
+    def rs_gemm_batched(self, rows: int, cols: int, dtype, nsamples: int, fns, fn_batched=None, q: int = 1,
+                        outs=None, run=None):
+        """rs_gemm_multi with ONE GEMM launch per owner sub-chunk for all samples:
+        fn_batched(s, D, d_planes, plane_div, planes_bs) (D: a tensor of the partial dtype) multiplies every (plane, sample) item at
+        once, batch b -> owner plane b / nsamples at sample b % nsamples of its region (sample
+        stride G * rows * cols elements: the per-sample regions of rs_gemm_multi)."""
+        if fn_batched is None:
+            return self.rs_gemm_multi(rows, cols, dtype, fns, q=q, outs=outs, run=run)
+        es = torch.empty((), dtype=dtype).element_size()
+        pbytes = rows * cols * es
+        off = self._region()
+        assert nsamples * self.G * pbytes <= self.scratch_bytes, "reduce-scatter region too small"
+        local = self._view(off, (self.G, rows, cols), dtype)  # (its dtype = the partial planes' dtype)
+        for s in range(q):
+            fn_batched(s, local[0], [self.base[j * q + s] + off + self.idx * pbytes for j in range(self.G // q)],
+                       nsamples, self.G * rows * cols)
+        self.bytes_sent += nsamples * (self.G - 1) * pbytes
+        self.barrier()
+        return [(self._view(off + k * self.G * pbytes, (self.G, rows, cols), dtype), self.G, rows * cols)
+                for k in range(nsamples)]
 
     def publish_all(self, hs) -> None:
         """One barrier publishes several producer-pushed gathers."""

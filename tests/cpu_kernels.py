@@ -101,7 +101,7 @@ def _apply_epilogue(v, ob, m, n, epi, alpha, d, ldd, d_bs, d2, ldd2, d2_bs, bias
 def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=False, epi=0, alpha=1.0, d2=None,
          bias=None, bias_bs=0, resid=None, r_bs=0, pre=None, p_bs=0, stats=None, stats_bs=0, d_bs=None,
          d2_bs=None, lda=None, ldb=None, ldd=None, a_lo=None, b_lo=None, adam=None, d_planes=None, d_bcast=None,
-         d2_bcast=None, rs=None, lnb=None):
+         d2_bcast=None, rs=None, lnb=None, plane_div=0, planes_bs=0):
     lda = lda if lda is not None else (k if am == KM else m)
     ldb = ldb if ldb is not None else (k if bm == KM else n)
     ldd = ldd if ldd is not None else n
@@ -138,9 +138,15 @@ def gemm(out, a, b, am, bm, m, n, k, batch=1, a_bs=0, b_bs=0, *, reduce_batch=Fa
     if rs is not None:
         return _gemm_rs(acc, out, m, n, ldd, d_planes, rs, epi, alpha, d2, bias, resid, pre, stats, d_bcast, d2_bcast)
     if d_planes:  # fused reduce-scatter: batch ob's partial goes straight to its owner's plane
-        assert epi == 0 and len(d_planes) >= len(acc)
+        assert epi == 0
+        es = torch.empty((), dtype=out.dtype).element_size()
         for ob, v in enumerate(acc):
-            _at(d_planes[ob], out.dtype, (m, n), (ldd, 1)).copy_((v * alpha).to(out.dtype))
+            if plane_div:  # batch ob -> plane ob // plane_div, sample ob % plane_div
+                addr = d_planes[ob // plane_div] + (ob % plane_div) * planes_bs * es
+            else:
+                assert len(d_planes) >= len(acc)
+                addr = d_planes[ob]
+            _at(addr, out.dtype, (m, n), (ldd, 1)).copy_((v * alpha).to(out.dtype))
         return out
     for ob, v in enumerate(acc):
         _apply_epilogue(v, ob, m, n, epi, alpha, out, ldd, d_bs, d2, n, d2_bs, bias, bias_bs, resid, n, r_bs,

@@ -247,7 +247,7 @@ def _run(world, r=1, mode="fwdbwd", opts=None):
     return sorted(res, key=lambda d: (d.get("rank", 0), d["pos"]))
 
 
-def _check(world, r=1, opts=None):
+def _check(world, r=1, opts=None, tol=1e-5):
     from oracle import model as om
     z = np.load(os.path.join(GOLD, "wm_golden.npz"))
     meta = json.load(open(os.path.join(GOLD, "comm_golden.json")))
@@ -267,13 +267,13 @@ def _check(world, r=1, opts=None):
         assert all((d["buf_peak"] > 0) == (R > 1) for d in res)
     for d in res:
         R, C, rr, cc = d["rc"]
-        assert rel_err(d["out"], om.local_sample(oc, ref_out, R, C, rr, cc)) < 1e-5
+        assert rel_err(d["out"], om.local_sample(oc, ref_out, R, C, rr, cc)) < tol
     for name in meta["param_names"]:
         gref = z[gpre + name]
         for d in res:
             R, C, rr, cc = d["rc"]
             tile = om.local_tile(oc, name, gref, R, C, rr, cc)
-            assert rel_err(d["grads"][name], tile) < 1e-5, (world, name, d["pos"], rel_err(d["grads"][name], tile))
+            assert rel_err(d["grads"][name], tile) < tol, (world, name, d["pos"], rel_err(d["grads"][name], tile))
 
 
 def test_single_rank_schedule_matches_reference():
@@ -558,3 +558,10 @@ def test_trainer_resume_reproduces_uninterrupted_run(world, tmp_path):
         assert d["resumed_rollouts"] == d["rollouts"]
         np.testing.assert_allclose(d["resumed"], d["full"], rtol=1e-6, atol=0)
         assert d["same_params"]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_bf16_batched_token_layers_peer_memory(world):
+    """bf16 operands and bf16 partial planes through the B > 1 plane-major path (batched
+    reduce-scatter GEMM launches, plane_div) on emulated peer memory, against the reference."""
+    _check(world, opts={"transport": "shm", "dtype": "bf16"}, tol=3e-2)
