@@ -124,6 +124,20 @@ if R * C > 1:
     run("epilogue_tok1", lambda: K.epilogue(hp, Er, Kl, acc_bs=Er * Kl, nplanes=R,
                                              epi=_lib.EPI_BIAS_COL | _lib.EPI_GELU_FWD, bias=b1, d=h, d2=a),
         Er * Kl * (2 * R + 4 + 2))
+    # channel layers: ch1 (col bias + GELU: bf16 pre-activation and activation), ch2 (col bias +
+    # residual + next LN moments, fp32 out)
+    Hl = H // C
+    cp = rnd(G, M, Hl, dtype=bf)
+    cpre = torch.empty(M, Hl, device=dev, dtype=bf)
+    cact = torch.empty(M, Hl, device=dev, dtype=bf)
+    bh = rnd(Hl)
+    run("epilogue_ch1", lambda: K.epilogue(cp, M, Hl, acc_bs=M * Hl, nplanes=G, epi=_lib.EPI_BIAS_COL | _lib.EPI_GELU_FWD,
+                                            bias=bh, d=cpre, d2=cact), M * Hl * (2 * G + 2 + 2))
+    yo = torch.empty(M, El, device=dev)
+    be = rnd(El)
+    run("epilogue_ch2", lambda: K.epilogue(planes, M, El, acc_bs=M * El, nplanes=G,
+                                            epi=_lib.EPI_BIAS_COL | _lib.EPI_RESID | _lib.EPI_STATS, bias=be,
+                                            resid=resid, d=yo, stats=stt), M * El * (2 * G + 4 + 4))
     red = torch.empty(M * El, device=dev)
     run("sum_planes", lambda: K.sum_planes(red, planes, M * El, G, M * El), M * El * (2 * G + 4))
 
