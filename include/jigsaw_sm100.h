@@ -181,6 +181,9 @@ int jg_sum_planes(float* y, const void* x, int32_t x_type, int64_t n, int32_t np
  * engines. */
 int jg_push(const void* src, int64_t bytes, const jg_bcast* dst, void* stream);
 int jg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* zero `bytes` of device memory (gradient / statistics accumulators at the start of a step;
+ * model.py:447-449 zero_grads) */
+int jg_memset(void* dst, int64_t bytes, void* stream);
 
 /* Device-side barrier of a Jigsaw group over peer memory (graph-capturable; publishes the
  * producer-push gathers and reduce-scatter partials of the exchanges in parallel.py:118-353).

@@ -34,7 +34,7 @@ EXPORTED = [
     "jg_gemm", "jg_split_tf32", "jg_split_tf32_2d", "jg_cast_bf16", "jg_gelu_fwd", "jg_gelu_bwd",
     "jg_ln_moments", "jg_ln_apply", "jg_ln_bwd_moments", "jg_ln_bwd_apply",
     "jg_colsum", "jg_rowsum", "jg_patchify", "jg_unpatchify", "jg_blend_loss",
-    "jg_adam", "jg_adam_sms", "jg_adam_push", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async", "jg_push",
+    "jg_adam", "jg_adam_sms", "jg_adam_push", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async", "jg_push", "jg_memset",
     "jg_group_barrier", "jg_opt_schedule", "jg_version", "jg_last_error", "jg_launch_count",
 ]
 JG_MAX_LR_CLASSES = 4
@@ -179,6 +179,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         "jg_sum_planes": [vp, vp, i32, i64, i32, i64, i32, vp],
         "jg_copy_async": [vp, vp, i64, vp],
         "jg_push": [vp, i64, vp, vp],
+        "jg_memset": [vp, i64, vp],
         "jg_group_barrier": [ctypes.POINTER(ctypes.c_void_p), vp, vp, i32, i32, vp],
     }
     for name, args in sig.items():

@@ -1358,6 +1358,11 @@ int jg_push(const void* src, int64_t bytes, const jg_bcast* dst, void* stream) {
   return JG_OK;
 }
 
+int jg_memset(void* dst, int64_t bytes, void* stream) {
+  if (bytes == 0) return JG_OK;
+  return jg::cuda_check(cudaMemsetAsync(dst, 0, (size_t)bytes, (cudaStream_t)stream), "cudaMemsetAsync");
+}
+
 int jg_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
   if (bytes == 0) return JG_OK;
   return jg::cuda_check(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream),

@@ -107,7 +107,7 @@ class TrainStep:
         if self.fused_adam or self.overwrite:
             for cls in f.CLASSES:  # matrix gradients are written whole by their GEMM; vectors accumulate
                 lo, hi = f.vec_range(cls)
-                f.grad[lo:hi].zero_()
+                K.zero(f.grad[lo:hi])
         else:
             m.zero_grads()
         m._panels_pushed = self._pushing()
@@ -119,7 +119,7 @@ class TrainStep:
     def _body_bwd(self) -> None:
         """Loss against the target, backward, gradient sync, Adam."""
         m, ws = self.model, self.ws
-        ws.loss.zero_()
+        K.zero(ws.loss)
         m._blend(ws, target=self.target, loss=ws.loss, loss_scale=self.loss_scale)
         if m.ctx.n > 1:
             m.ctx.all_reduce_all(ws.loss)  # the loss is a sum of per-tile terms
@@ -187,7 +187,7 @@ class TrainStep:
         mp group, duplicated vectors counted once (weight 1/R for column vectors shared by the
         column group, 1/C for the row vector shared by the row group; parallel.py:483-485)."""
         m, f = self.model, self.model.flat
-        self.sqsum.zero_()
+        K.zero(self.sqsum)
         for cls in f.CLASSES:
             for kind, w in (("matrix", 1.0), ("vec_col", 1.0 / m.R), ("vec_row", 1.0 / m.C)):
                 lo, hi = f.kind_range[(cls, kind)]

@@ -601,7 +601,7 @@ def forward_grid(m, ws) -> None:
     M = B * Tl
     lat, lon = m.local_grid
     od = m.op_dtype
-    ws.stats.zero_()
+    K.zero(ws.stats)
     if getattr(m, "_panels_pushed", False) and g.kind == "symm" and g.panel_names:
         panels_ready(m, g)
     else:
@@ -645,7 +645,7 @@ def backward_grid(m, ws) -> None:
     Tl, El, Er, Kl, Hl, Fl = ws.Tl, ws.El, ws.Er, ws.Kl, ws.Hl, ws.Fl
     M = B * Tl
     od = m.op_dtype
-    ws.bstats.zero_()
+    K.zero(ws.bstats)
     gf = ws.g
     # decoder: g = gd Wdec, its operand copy pushed to the row group for ch2's backward
     hg = g.row.dest((M, El), od, slot="g")

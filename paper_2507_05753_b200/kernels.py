@@ -63,6 +63,12 @@ def copy_async(dst_ptr: int, src: torch.Tensor, nbytes: int | None = None):
     _lib.call("jg_copy_async", dst_ptr, src.data_ptr(), nbytes if nbytes is not None else src.numel() * src.element_size())
 
 
+def zero(t: torch.Tensor):
+    """Zero a contiguous tensor (jg_memset; accumulators at the start of a step)."""
+    assert t.is_contiguous()
+    _lib.call("jg_memset", t.data_ptr(), t.numel() * t.element_size())
+
+
 def push(src: torch.Tensor, addrs, nbytes: int | None = None):
     """SM-driven copy of `src` to up to 4 raw device addresses (own / NVLink peer memory)."""
     _lib.call("jg_push", src.data_ptr(), nbytes if nbytes is not None else src.numel() * src.element_size(),

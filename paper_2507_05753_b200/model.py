@@ -425,7 +425,7 @@ class WeatherMixerModel:
         Tn, E, F, Kd, H = cfg.tokens, cfg.d_emb, cfg.patch_features, cfg.d_tok, cfg.d_ch
         lat, lon = self.local_grid
         M = B * Tn
-        ws.stats.zero_()
+        K.zero(ws.stats)
         K.patchify(ws.xin, ws.xp, B, lat, lon, cfg.n_vars, cfg.patch[0], cfg.patch[1])
         # encoder: res0 = xp Wenc^T + benc, with LN1 moments of block 0
         self._gemm(ws.res[0], ws.xp, p["enc.w"].op, KM, KM, M, E, F, epi=E_BCOL | E_ST,
@@ -521,7 +521,7 @@ class WeatherMixerModel:
         cfg, p, B = self.cfg, self.params, ws.B
         Tn, E, F, Kd, H = cfg.tokens, cfg.d_emb, cfg.patch_features, cfg.d_tok, cfg.d_ch
         M = B * Tn
-        ws.bstats.zero_()
+        K.zero(ws.bstats)
         # decoder (NT): g = gd Wdec ; dW += gd^T y ; db += sum gd
         g, g_op = ws.g, ws.g_op
         self._gemm(g, ws.gd, p["dec.w"].op, KM, MN, M, E, F, epi=0 if g_op is g else E_CP,

@@ -98,7 +98,8 @@ class FlatParams:
             self.params[name] = p
 
     def zero_grads(self) -> None:
-        self.grad.zero_()
+        from . import kernels as K  # (jg_memset: one launch for every gradient of the model)
+        K.zero(self.grad)
 
     def view(self, name: str, buf: torch.Tensor) -> torch.Tensor:
         """`name`'s view into another flat buffer (m, v, ...) with the same layout."""

@@ -245,6 +245,10 @@ def _unpatchify(tok, batch, lat, lon, chans, pl, pw):
     return t.reshape(batch, lat, lon, chans)
 
 
+def zero(t):
+    t.zero_()
+
+
 def push(src, addrs, nbytes=None):
     for a in addrs or []:
         copy_async(a, src, nbytes)
@@ -408,7 +412,7 @@ def step_increment(counter):
 
 NAMES = ["gemm", "epilogue", "sum_planes", "axpy", "cast_bf16", "patchify", "ln_moments", "ln_apply", "ln_bwd_moments",
          "ln_bwd_apply", "colsum", "rowsum", "blend_loss", "adam", "step_increment", "sqnorm", "opt_schedule",
-         "copy_async", "gelu_fwd", "gelu_bwd", "push"]
+         "copy_async", "gelu_fwd", "gelu_bwd", "push", "zero"]
 
 
 def install():
