@@ -63,9 +63,15 @@ def copy_async(dst_ptr: int, src: torch.Tensor, nbytes: int | None = None):
     _lib.call("jg_copy_async", dst_ptr, src.data_ptr(), nbytes if nbytes is not None else src.numel() * src.element_size())
 
 
+_TORCH_ZERO = __import__("os").environ.get("JIGSAW_TORCH_ZERO") == "1"  # A/B only
+
+
 def zero(t: torch.Tensor):
     """Zero a contiguous tensor (jg_memset; accumulators at the start of a step)."""
     assert t.is_contiguous()
+    if _TORCH_ZERO:
+        t.zero_()
+        return
     _lib.call("jg_memset", t.data_ptr(), t.numel() * t.element_size())
 
 
