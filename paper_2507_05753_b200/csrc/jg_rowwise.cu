@@ -789,8 +789,14 @@ struct EpiArgs {
   Bcast dbc, d2bc;
 };
 
+// F: the epilogue flags when known at compile time (EPI_DYN: read a.epi). With constant flags the
+// operand loads are unconditional, so the compiler issues them together (one memory round trip
+// per unit) and allocates registers only for the operands in use.
+constexpr uint32_t EPI_DYN = 0xFFFFFFFFu;
+template <uint32_t F = EPI_DYN>
 __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t r, int64_t c, float rb, float* v,
                                            float& s1, float& s2) {
+  const uint32_t epi = F == EPI_DYN ? a.epi : F;
   if (a.nplanes > 1) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = 0.f;
@@ -806,23 +812,23 @@ __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t 
   float t[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = v[k] * a.alpha + rb;
-  if (a.epi & JG_EPI_BIAS_COL) {
+  if (epi & JG_EPI_BIAS_COL) {
     jgd::load8(a.bias, b * a.bias_bs + c, false, t);
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] += t[k];
   }
-  if (a.epi & JG_EPI_RESID) {
+  if (epi & JG_EPI_RESID) {
     jgd::load8(a.resid, b * a.r_bs + r * a.ldr + c, false, t);
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] += t[k];
   }
-  if (a.epi & JG_EPI_GELU_BWD) {
+  if (epi & JG_EPI_GELU_BWD) {
     jgd::load8(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16, t);
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] *= jgd::gelu_grad_f(t[k]);
   }
   const int64_t od = b * a.d_bs + r * a.ldd + c;
-  if (a.epi & JG_EPI_ACCUM) {
+  if (epi & JG_EPI_ACCUM) {
     jgd::load8(a.d, od, false, t);
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] += t[k];
@@ -833,8 +839,8 @@ __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t 
     s2 += v[k] * v[k];
   }
   if (a.d) store8_bc(a.d, a.dbc, od, a.d_bf16, v);
-  if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
-    if (a.epi & JG_EPI_GELU_FWD) {
+  if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2)) {
+    if (epi & JG_EPI_GELU_FWD) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) t[k] = jgd::gelu_f(v[k]);
       store8_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, t);
@@ -847,7 +853,9 @@ __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t 
 // Vector path: warp unit = (row, 256-column chunk), so even a few thousand rows give tens of
 // thousands of independent units (enough loads in flight without long per-warp row loops);
 // LN-moment partials are warp-reduced per unit and added with one atomic pair per unit.
+template <uint32_t F = EPI_DYN>
 __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
+  const uint32_t epi = F == EPI_DYN ? a.epi : F;
   const int64_t b = blockIdx.y;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -856,13 +864,13 @@ __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
     const int64_t nch = (a.n + 255) / 256;
     for (int64_t u = wid; u < a.m * nch; u += warps) {
       const int64_t r = u / nch, c = (u - r * nch) * 256 + lane * 8;
-      const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
+      const float rb = (epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
       float s1 = 0.f, s2 = 0.f;
       if (c < a.n) {
         float v[8];
-        epi_apply8(a, b, r, c, rb, v, s1, s2);
+        epi_apply8<F>(a, b, r, c, rb, v, s1, s2);
       }
-      if (a.epi & JG_EPI_STATS) {
+      if (epi & JG_EPI_STATS) {
         s1 = warp_sum(s1);
         s2 = warp_sum(s2);
         if (lane == 0) {
@@ -875,7 +883,7 @@ __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
     return;
   }
   for (int64_t r = wid; r < a.m; r += warps) {
-    const float rb = (a.epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
+    const float rb = (epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
     float s1 = 0.f, s2 = 0.f;
     for (int64_t c = lane; c < a.n; c += 32) {
       float v = 0.f;
@@ -885,18 +893,18 @@ __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
         v = jgd::load1(a.acc, b * a.a_bs + r * a.lda + c, a.acc_bf16);
       }
       v = v * a.alpha + rb;
-      if (a.epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
-      if (a.epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
-      if (a.epi & JG_EPI_GELU_BWD) v *= jgd::gelu_grad_f(jgd::load1(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16));
+      if (epi & JG_EPI_BIAS_COL) v += a.bias[b * a.bias_bs + c];
+      if (epi & JG_EPI_RESID) v += a.resid[b * a.r_bs + r * a.ldr + c];
+      if (epi & JG_EPI_GELU_BWD) v *= jgd::gelu_grad_f(jgd::load1(a.pre, b * a.p_bs + r * a.ldp + c, a.pre_bf16));
       const int64_t od = b * a.d_bs + r * a.ldd + c;
-      if (a.epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
+      if (epi & JG_EPI_ACCUM) v += reinterpret_cast<const float*>(a.d)[od];
       s1 += v;
       s2 += v * v;
       if (a.d) store1_bc(a.d, a.dbc, od, a.d_bf16, v);
-      if (a.epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
-        store1_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (a.epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
+      if (epi & (JG_EPI_GELU_FWD | JG_EPI_COPY_D2))
+        store1_bc(a.d2, a.d2bc, b * a.d2_bs + r * a.ldd2 + c, a.d2_bf16, (epi & JG_EPI_GELU_FWD) ? jgd::gelu_f(v) : v);
     }
-    if (a.epi & JG_EPI_STATS) {
+    if (epi & JG_EPI_STATS) {
       s1 = warp_sum(s1);
       s2 = warp_sum(s2);
       if (lane == 0) {
@@ -1282,8 +1290,23 @@ int jg_epilogue(const jg_gemm_desc* g, const void* acc, int32_t acc_type, int64_
                    a16(g->d2) && a16(g->bias) && a16(g->resid) && a16(g->pre) && g->d_bstride % 8 == 0 &&
                    g->r_bstride % 8 == 0 && g->p_bstride % 8 == 0 && g->d2_bstride % 8 == 0;
   const int64_t units = vec ? g->m * ((g->n + 255) / 256) : g->m;  // warp units per batch entry
-  dim3 grid((unsigned)resident_grid(epilogue_kernel, 256, (units + 7) / 8), (unsigned)g->batch);
-  epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a, vec);
+  // the flag sets of the Jigsaw step get their own instantiation (loads issued together)
+  auto launch = [&](auto kern) {
+    dim3 grid((unsigned)resident_grid(kern, 256, (units + 7) / 8), (unsigned)g->batch);
+    kern<<<grid, 256, 0, (cudaStream_t)stream>>>(a, vec);
+  };
+  switch (g->epi) {
+    case JG_EPI_BIAS_ROW | JG_EPI_RESID | JG_EPI_STATS: launch(epilogue_kernel<JG_EPI_BIAS_ROW | JG_EPI_RESID | JG_EPI_STATS>); break;
+    case JG_EPI_BIAS_COL | JG_EPI_GELU_FWD: launch(epilogue_kernel<JG_EPI_BIAS_COL | JG_EPI_GELU_FWD>); break;
+    case JG_EPI_BIAS_COL | JG_EPI_RESID | JG_EPI_STATS: launch(epilogue_kernel<JG_EPI_BIAS_COL | JG_EPI_RESID | JG_EPI_STATS>); break;
+    case JG_EPI_BIAS_COL | JG_EPI_RESID: launch(epilogue_kernel<JG_EPI_BIAS_COL | JG_EPI_RESID>); break;
+    case JG_EPI_BIAS_COL | JG_EPI_RESID | JG_EPI_COPY_D2: launch(epilogue_kernel<JG_EPI_BIAS_COL | JG_EPI_RESID | JG_EPI_COPY_D2>); break;
+    case JG_EPI_BIAS_COL | JG_EPI_STATS: launch(epilogue_kernel<JG_EPI_BIAS_COL | JG_EPI_STATS>); break;
+    case JG_EPI_BIAS_COL: launch(epilogue_kernel<JG_EPI_BIAS_COL>); break;
+    case JG_EPI_GELU_BWD: launch(epilogue_kernel<JG_EPI_GELU_BWD>); break;
+    case 0: launch(epilogue_kernel<0u>); break;
+    default: launch(epilogue_kernel<EPI_DYN>); break;
+  }
   JG_LAUNCH_CHECK("epilogue");
   return JG_OK;
 }
