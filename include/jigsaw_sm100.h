@@ -19,6 +19,7 @@
 #ifndef JIGSAW_SM100_H
 #define JIGSAW_SM100_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -150,6 +151,9 @@ typedef struct jg_gemm_desc {
    * sample of a Jigsaw token layer (parallel.py:118-132 per sample). TMA-store epilogue only. */
   int32_t plane_div;
   int64_t d_planes_bstride;
+  /* output tile width: 0 = chosen per shape (wave-quantisation model), else 64 / 128 / 256
+   * (64 only for problems of at most 128 rows: CTA pairs need 128 or 256) */
+  int32_t tile_n;
 } jg_gemm_desc;
 
 int jg_gemm(const jg_gemm_desc* desc, void* stream);
@@ -320,6 +324,8 @@ const char* jg_version(void);
 const char* jg_last_error(void);
 /* number of kernels launched by this library since load (evidence counter for bench.py). */
 int64_t jg_launch_count(void);
+/* sizeof(jg_gemm_desc): bindings check their struct mirror against it at load time. */
+size_t jg_gemm_desc_size(void);
 
 #pragma GCC visibility pop
 #ifdef __cplusplus

@@ -36,6 +36,7 @@ EXPORTED = [
     "jg_colsum", "jg_rowsum", "jg_patchify", "jg_unpatchify", "jg_blend_loss",
     "jg_adam", "jg_adam_sms", "jg_adam_push", "jg_step_increment", "jg_sqnorm", "jg_epilogue", "jg_axpy", "jg_sum_planes", "jg_copy_async", "jg_push", "jg_memset",
     "jg_group_barrier", "jg_opt_schedule", "jg_version", "jg_last_error", "jg_launch_count",
+    "jg_gemm_desc_size",
 ]
 JG_MAX_LR_CLASSES = 4
 
@@ -133,6 +134,7 @@ class GemmDesc(ctypes.Structure):
         ("lnb_gamma", ctypes.c_void_p), ("lnb_mr", ctypes.c_void_p),
         ("max_sms", ctypes.c_int32),
         ("plane_div", ctypes.c_int32), ("d_planes_bstride", ctypes.c_int64),
+        ("tile_n", ctypes.c_int32),
     ]
 
 
@@ -189,6 +191,10 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     lib.jg_version.restype = ctypes.c_char_p
     lib.jg_last_error.restype = ctypes.c_char_p
     lib.jg_launch_count.restype = ctypes.c_int64
+    lib.jg_gemm_desc_size.restype = ctypes.c_size_t
+    if lib.jg_gemm_desc_size() != ctypes.sizeof(GemmDesc):
+        raise RuntimeError(f"{path}: jg_gemm_desc is {lib.jg_gemm_desc_size()} bytes in the library, "
+                           f"{ctypes.sizeof(GemmDesc)} in _lib.GemmDesc (stale build?)")
     _lib = lib
     return lib
 

@@ -41,4 +41,6 @@ const char* jg_last_error(void) { return jg::t_last_error.c_str(); }
 
 int64_t jg_launch_count(void) { return jg::g_launches.load(std::memory_order_relaxed); }
 
+size_t jg_gemm_desc_size(void) { return sizeof(jg_gemm_desc); }
+
 }  // extern "C"

@@ -968,6 +968,11 @@ extern "C" int jg_gemm(const jg_gemm_desc* g, void* stream_v) {
     const int64_t t256 = mt * ((g->n + 255) / 256) * out_batches;
     if (t256 < jg::num_sms() / cg) bn = 128;
   }
+  if (g->tile_n != 0) {
+    JG_SHAPE_CHECK(g->tile_n == 256 || g->tile_n == 128 || (g->tile_n == 64 && cg == 1),
+                   "jg_gemm: tile_n must be 0, 64 (at most 128 rows), 128 or 256");
+    bn = g->tile_n;
+  }
   p.m_tiles = static_cast<int>(mt);
   p.n_tiles = static_cast<int>((g->n + bn - 1) / bn);
   const int64_t nt = static_cast<int64_t>(p.m_tiles) * p.n_tiles * out_batches;

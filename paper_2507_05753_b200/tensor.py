@@ -34,6 +34,10 @@ GEMM_TIMER: list | None = None
 # GEMMs leave SMs free for the optimiser of the blocks already finished (engine.TrainStep).
 GEMM_SM_CAP = 0
 
+# Output tile width for the GEMMs issued while it is set (0: chosen per shape by jg_gemm;
+# tools/tile_n_probe.py A/B-tests the choice).
+GEMM_TILE_N = 0
+
 # 3xTF32 K-chunking (fp32 mode). tcgen05's fp32 accumulation of each MMA step is not
 # round-to-nearest: its error grows ~ K^1.5 (relative ~1.3e-8 * K measured on B200,
 # tools/f32_diag.py: 2e-6 at K = 64, 2.2e-4 at K = 16380). fp32-mode GEMMs with K above
@@ -129,6 +133,7 @@ def gemm_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor, a_major: int,
     d.ldb = ldb if ldb is not None else (k if b_major == _lib.JG_KMAJOR else n)
     d.epi, d.alpha = epi, alpha
     d.max_sms = GEMM_SM_CAP
+    d.tile_n = GEMM_TILE_N
     d.d, d.ldd, d.d_type = _lib.ptr(out), ldd if ldd is not None else n, _lib.dtype_code(out) if out is not None else 0
     d.d_bstride = d_bs if d_bs is not None else (0 if reduce_batch else m * n)
     if d2 is not None:

@@ -16,7 +16,7 @@ LIB = os.path.join(ROOT, "paper_2507_05753_b200", "libjigsaw_sm100.so")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|int64_t)\s+(jg_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|int64_t|size_t)\s+(jg_\w+)\s*\(", text, re.M)))
 
 
 @pytest.fixture(scope="module")
@@ -63,3 +63,11 @@ def test_shape_errors_raise_before_launch(lib):
                     "jg_ln_apply")
     with pytest.raises(ShapeError, match="not divisible"):
         _lib._check(_lib.load().jg_patchify(None, None, 0, 1, 5, 8, 2, 2, 2, None), "jg_patchify")
+
+
+def test_gemm_desc_layout_matches_binding(lib):
+    """The ctypes mirror of jg_gemm_desc has the library's size (a stale .so or a field added on
+    one side only is caught at load time by _lib.load, and here without a GPU)."""
+    from paper_2507_05753_b200 import _lib
+    lib.jg_gemm_desc_size.restype = ctypes.c_size_t
+    assert lib.jg_gemm_desc_size() == ctypes.sizeof(_lib.GemmDesc)

@@ -216,3 +216,31 @@ def test_tf32x3_long_k_lnb_and_reduce_batch(cuda):
                 epi=_lib.EPI_ACCUM)
     want = torch.einsum("bte,bej->tj", u.double(), gh.double())
     assert rel_err(dw.cpu().numpy(), want.cpu().numpy()) < 2e-5
+
+
+@pytest.mark.parametrize("tile_n", [128, 256])
+@pytest.mark.parametrize("majors", [(0, 0), (1, 1)])
+def test_forced_tile_width_same_result(cuda, tile_n, majors):
+    """jg_gemm_desc.tile_n (forced 128- / 256-wide tiles on CTA pairs) gives the per-shape
+    choice's result bit for bit (the K loop order per output element does not change)."""
+    from paper_2507_05753_b200 import ShapeError, tensor as T
+    m, n, k = 520, 776, 384
+    g = torch.Generator(device="cpu").manual_seed(11)
+    am, bm = majors
+    a = torch.randn((m, k) if am == 0 else (k, m), generator=g).to(cuda, torch.bfloat16)
+    b = torch.randn((n, k) if bm == 0 else (k, n), generator=g).to(cuda, torch.bfloat16)
+    auto = torch.empty(m, n, device=cuda)
+    T.gemm_into(auto, a, b, am, bm, m, n, k)
+    forced = torch.empty_like(auto)
+    try:
+        T.GEMM_TILE_N = tile_n
+        T.gemm_into(forced, a, b, am, bm, m, n, k)
+        T.GEMM_TILE_N = 64  # CTA pairs need 128- or 256-wide tiles
+        with pytest.raises(ShapeError):
+            T.gemm_into(forced, a, b, am, bm, m, n, k)
+    finally:
+        T.GEMM_TILE_N = 0
+    torch.cuda.synchronize()
+    assert torch.equal(forced, auto)
+    ref = (a.double().cpu() if am == 0 else a.double().cpu().T) @ (b.double().cpu().T if bm == 0 else b.double().cpu())
+    assert rel_err(auto.cpu().numpy(), ref.numpy()) < 1e-2
