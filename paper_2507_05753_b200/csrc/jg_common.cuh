@@ -223,10 +223,37 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_byte
 }
 
 // --- math ---
-__device__ __forceinline__ float gelu_f(float x) { return x * 0.5f * (1.0f + erff(x * 0.70710678118654752f)); }
+#ifndef JG_GELU_FAST
+#define JG_GELU_FAST 1
+#endif
+// Phi(x) = 0.5 (1 + erf(x / sqrt 2)) and (for the GELU gradient) phi(x) = exp(-x^2/2) / sqrt(2 pi).
+// JG_GELU_FAST=1 (default): Abramowitz & Stegun 7.1.26 for erf (|error| <= 6e-7 absolute in fp32
+// arithmetic), branch-free — one MUFU reciprocal, one MUFU exp shared with phi, five FMAs; 16 %
+// faster Jigsaw GELU / GELU' epilogues than libdevice erff (tools/membench.py, r3j). =0: erff.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float gelu_cdf(float x, float* pdf) {
+#if JG_GELU_FAST == 1
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
+  const float poly = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
+                              0.254829592f);
+  const float e = __expf(-z * z);  // = exp(-x^2 / 2)
+  if (pdf) *pdf = e * 0.3989422804014327f;
+  const float half_erfc = 0.5f * poly * e;  // 0.5 (1 - erf(|x| / sqrt 2))
+  return x >= 0.f ? 1.0f - half_erfc : half_erfc;
+#else
+  if (pdf) *pdf = __expf(-0.5f * x * x) * 0.3989422804014327f;
+  return 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+#endif
+}
+__device__ __forceinline__ float gelu_f(float x) { return x * gelu_cdf(x, nullptr); }
 __device__ __forceinline__ float gelu_grad_f(float x) {
-  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
-  const float pdf = __expf(-0.5f * x * x) * 0.3989422804014327f;
+  float pdf;
+  const float cdf = gelu_cdf(x, &pdf);
   return cdf + x * pdf;
 }
 

@@ -862,7 +862,8 @@ __global__ void epilogue_kernel(const EpiArgs a, bool vec) {
   const int lane = threadIdx.x & 31;
   if (vec) {
     const int64_t nch = (a.n + 255) / 256;
-    for (int64_t u = wid; u < a.m * nch; u += warps) {
+    const int64_t units = a.m * nch;
+    for (int64_t u = wid; u < units; u += warps) {
       const int64_t r = u / nch, c = (u - r * nch) * 256 + lane * 8;
       const float rb = (epi & JG_EPI_BIAS_ROW) ? a.bias[b * a.bias_bs + r] : 0.f;
       float s1 = 0.f, s2 = 0.f;

@@ -133,6 +133,10 @@ if R * C > 1:
     bh = rnd(Hl)
     run("epilogue_ch1", lambda: K.epilogue(cp, M, Hl, acc_bs=M * Hl, nplanes=G, epi=_lib.EPI_BIAS_COL | _lib.EPI_GELU_FWD,
                                             bias=bh, d=cpre, d2=cact), M * Hl * (2 * G + 2 + 2))
+    # backward GELU' epilogue (ch2 dX form): sum of planes * gelu'(pre) -> bf16 gradient
+    gco = torch.empty(M, Hl, device=dev, dtype=bf)
+    run("epilogue_gb", lambda: K.epilogue(cp, M, Hl, acc_bs=M * Hl, nplanes=G, epi=_lib.EPI_GELU_BWD, pre=cpre, d=gco),
+        M * Hl * (2 * G + 2 + 2))
     yo = torch.empty(M, El, device=dev)
     be = rnd(El)
     run("epilogue_ch2", lambda: K.epilogue(planes, M, El, acc_bs=M * El, nplanes=G,
