@@ -115,17 +115,22 @@ def test_bench_dp_replicas(n, mp):
     assert abs(d["value"] - (n // mp) * 1000.0 / d["ms_per_step"]) < 1e-6 * d["value"]
 
 
-@pytest.mark.parametrize("n", [2, 4])
-def test_jigsaw_matches_single_gpu_at_c4_scale(n):
+@pytest.mark.parametrize("n,grid", [(2, None), (4, None), (4, "4x1")])
+def test_jigsaw_matches_single_gpu_at_c4_scale(n, grid):
     """At the benchmarked C4 geometry (one block, bf16): every rank's tiles of the sharded output
-    and parameter gradients agree with the single-GPU run to the bf16 tolerance (north_star)."""
+    and parameter gradients agree with the single-GPU run to the bf16 tolerance (north_star).
+    4x1: four longitude splits as in the 8-GPU 4x2 grid — 4095 tokens per rank (odd row counts
+    in every token-dimension TMA map) and q = 4 owner sub-chunks, at full scale."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", "--master-port=29571", os.path.join(HERE, "mp_c4_check.py")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    env = dict(os.environ, JIGSAW_GRID=grid) if grid else None
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     line = [ln for ln in p.stdout.splitlines() if ln.startswith("MPC4 ")]
     assert p.returncode == 0 and line, p.stdout[-3000:] + p.stderr[-3000:]
     res = json.loads(line[0][len("MPC4 "):])
     print(res)
+    if grid:
+        assert res["grid"] == [int(v) for v in grid.split("x")]
     assert res["out"] < 2e-2 and res["grad"] < 2e-2, res
