@@ -151,6 +151,11 @@ class ClockSampler:
                 time.sleep(0.001)
             self.samples.clear()
             self.source = "nvml"
+            try:  # board energy over the region (mJ counter): J per step under the 1 kW cap
+                self._nv, self._h = nv, h
+                self._e0, self._t0 = nv.nvmlDeviceGetTotalEnergyConsumption(h), time.time()
+            except Exception:  # noqa: BLE001
+                self._e0 = None
         except Exception:  # noqa: BLE001
             self.source = "nvidia-smi"
             try:
@@ -169,6 +174,14 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self._stop.set()
+        self.energy_j = self.avg_power_w = None
+        if getattr(self, "_e0", None) is not None:
+            try:
+                de = (self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h) - self._e0) / 1e3
+                dt = time.time() - self._t0
+                self.energy_j, self.avg_power_w = de, (de / dt if dt > 0 else None)
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -195,8 +208,12 @@ class ClockSampler:
             for nm, v in zip(self.NAMES, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "source": self.source}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+               "samples": len(sm), "source": self.source}
+        if getattr(self, "energy_j", None) is not None:
+            out["energy_j"] = round(self.energy_j, 3)  # this GPU, whole timed region (NVML counter)
+            out["avg_power_w"] = round(self.avg_power_w, 1) if self.avg_power_w else None
+        return out
 
 
 def cpu_reference_sample(cfg_kw, lat_real, vars_real, batch):
@@ -369,6 +386,8 @@ def run_ours(args, rank, world):
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     clock = clocks.summary()
+    if clock.get("energy_j") is not None:
+        clock["energy_j_per_step"] = round(clock["energy_j"] / args.steps, 3)
     loss_val = float(step.ws.loss.item())
 
     # ---------------- e2e: public API with pinned host buffers ---------------------------
