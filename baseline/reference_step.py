@@ -107,10 +107,37 @@ class ReferenceStep:
         return self.ctx.flops
 
 
+def blas_threads(n: int):
+    """Context that runs numpy's BLAS on n threads. torchrun exports OMP_NUM_THREADS=1 to every
+    rank, which OpenBLAS reads at load time; the reference arm (rank 0 alone) should use all the
+    host threads whatever the launcher, so the pool is resized at run time (threadpoolctl)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n, user_api="blas")
+    except Exception:  # noqa: BLE001
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def blas_thread_count() -> int | None:
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads") or 0) for i in threadpool_info() if i.get("user_api") == "blas") or None
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def time_steps(cfg_kw, lat_real, vars_real, batch, warmup, steps, budget_s):
     """(per-step seconds list, warm-ups actually run, init seconds, loss) — warm-up and timed
-    steps are capped so the whole run stays inside budget_s (estimated from the first step)."""
+    steps are capped so the whole run stays inside budget_s (estimated from the first step).
+    BLAS runs on every host thread (see blas_threads)."""
+    with blas_threads(host_cores()):
+        return _time_steps(cfg_kw, lat_real, vars_real, batch, warmup, steps, budget_s)
+
+
+def _time_steps(cfg_kw, lat_real, vars_real, batch, warmup, steps, budget_s):
     rs = ReferenceStep(cfg_kw, lat_real, vars_real, batch)
+    rs.blas_threads = blas_thread_count()  # the pool size the timed steps actually ran with
     times, warm_done, loss = [], 0, float("nan")
     t_first = None
     for _ in range(max(0, warmup)):

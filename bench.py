@@ -231,6 +231,7 @@ def cpu_reference_sample(cfg_kw, lat_real, vars_real, batch):
         full = om.Config(**{k: v for k, v in cfg_kw.items() if k != "dropout_rate"})
         scale = om.train_flops(full, batch) / rs.flops()
         t_step = times[0] * scale
+        cores = getattr(rs, "blas_threads", None) or cores
         return {"value": batch / t_step, "unit": "samples/s", "cores": cores, "kind": "reference",
                 "sample": f"one training step (zero_grads, forward, SPEC loss, backward, grad_sync, Adam) of the "
                           f"unmodified reference package (baseline/_ref, f32 numpy/OpenBLAS, {cores} threads, "
@@ -263,7 +264,7 @@ def run_reference(args, rank, world):
                                                    args.steps, budget)
     t_step = statistics.median(times)
     value = args.batch / t_step
-    cores = rsm.host_cores()
+    cores = getattr(rs, "blas_threads", None) or rsm.host_cores()
     oc = om.Config(**{k: v for k, v in cfg_kw.items() if k != "dropout_rate"})
     flops = om.train_flops(oc, args.batch)
     sample = (f"full training steps of the unmodified reference package (baseline/_ref jigsaw 0.1.0, n = 1, f32 "
