@@ -264,16 +264,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   static_assert(CG == 1 || !TF32, "2-CTA path is bf16 only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-#ifdef JG_SMEM_INTERLEAVE
-  // experiment: stage-major layout [A0 B0][A1 B1]... (A and B of one stage adjacent)
-  uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + C::A_BYTES;
-  constexpr int A_STRIDE = C::STAGE_BYTES, B_STRIDE = C::STAGE_BYTES;
-#else
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
   constexpr int A_STRIDE = C::A_BYTES, B_STRIDE = C::B_BYTES;
-#endif
   uint8_t* smem_epi = smem + C::STAGES * C::STAGE_BYTES;  // 1024-aligned: 4 x 4 KB staging tiles
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + C::EPI_STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
@@ -816,11 +809,7 @@ int make_operand_map(CUtensorMap* map, const void* ptr, bool tf32, bool mn_major
     jg::set_error("cuTensorMapEncodeTiled unavailable (driver entry point lookup failed)");
     return JG_ERR_CUDA;
   }
-#ifdef JG_MN_L2PROMO
-  const CUtensorMapL2promotion promo = mn_major ? (CUtensorMapL2promotion)JG_MN_L2PROMO : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-#else
   const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-#endif
   CUresult r = fn(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -651,9 +651,6 @@ __device__ __forceinline__ void push_bf16x1(const jg_push_table& t, int64_t e, _
   }
 }
 
-#ifndef JG_ADAM_CS
-#define JG_ADAM_CS 0
-#endif
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, __nv_bfloat16* __restrict__ pb, int64_t n, float lr, float b1,
                             float b2, float eps, const int32_t* __restrict__ step, const float* __restrict__ gscale,
@@ -665,17 +662,10 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
   const float s = gscale ? *gscale : 1.0f;
   const int64_t n4 = n / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-#if JG_ADAM_CS  // streaming (evict-first) loads / stores: every byte is touched once per step
-    float4 pp = __ldcs(reinterpret_cast<const float4*>(p) + i);
-    const float4 gg = __ldcs(reinterpret_cast<const float4*>(g) + i);
-    float4 mm = __ldcs(reinterpret_cast<const float4*>(m) + i);
-    float4 vv = __ldcs(reinterpret_cast<const float4*>(v) + i);
-#else
     float4 pp = reinterpret_cast<float4*>(p)[i];
     const float4 gg = reinterpret_cast<const float4*>(g)[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
     float4 vv = reinterpret_cast<float4*>(v)[i];
-#endif
     float* pa = &pp.x; const float* ga = &gg.x; float* ma = &mm.x; float* va = &vv.x;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -684,15 +674,9 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
       va[j] = b2 * va[j] + (1.0f - b2) * gj * gj;
       pa[j] -= lr * (ma[j] * bc1) / (sqrtf(va[j] * bc2) + eps);
     }
-#if JG_ADAM_CS
-    __stcs(reinterpret_cast<float4*>(p) + i, pp);
-    __stcs(reinterpret_cast<float4*>(m) + i, mm);
-    __stcs(reinterpret_cast<float4*>(v) + i, vv);
-#else
     reinterpret_cast<float4*>(p)[i] = pp;
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
-#endif
     if (pb) {
       __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y), hi = __floats2bfloat162_rn(pp.z, pp.w);
       uint2 raw;
