@@ -837,8 +837,18 @@ __device__ __forceinline__ void epi_apply8(const EpiArgs& a, int64_t b, int64_t 
 // Vector path: warp unit = (row, 256-column chunk), so even a few thousand rows give tens of
 // thousands of independent units (enough loads in flight without long per-warp row loops);
 // LN-moment partials are warp-reduced per unit and added with one atomic pair per unit.
+// Minimum resident blocks per SM (register cap) per flag set, from A/Bs of 1 / 6 / 8 on 2x2 tiles
+// (tools/membench.py; profiles/r2/r3x_epilogue_minblocks.log, r3y_epilogue_bounds_vs_none.log):
+// against no launch bounds, the residual + moments forms gain 6-8 %, GELU' 9 %, GELU 5-15 %.
+template <uint32_t F>
+constexpr int epi_min_blocks() {
+  return F == (JG_EPI_BIAS_ROW | JG_EPI_RESID | JG_EPI_STATS)   ? 8
+         : F == (JG_EPI_BIAS_COL | JG_EPI_RESID | JG_EPI_STATS) ? 6
+         : F == JG_EPI_GELU_BWD                                  ? 6
+                                                                 : 1;
+}
 template <uint32_t F = EPI_DYN>
-__global__ void epilogue_kernel(const EpiArgs a, bool vec) {
+__global__ void __launch_bounds__(256, epi_min_blocks<F>()) epilogue_kernel(const EpiArgs a, bool vec) {
   const uint32_t epi = F == EPI_DYN ? a.epi : F;
   const int64_t b = blockIdx.y;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
