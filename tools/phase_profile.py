@@ -1,4 +1,5 @@
-"""Per-call CUDA-event breakdown of one eager training step (rank 0 prints), under torchrun or alone."""
+"""Per-call CUDA-event breakdown of one eager training step (rank 0 prints), under torchrun or alone.
+COPY_SITES=1 also lists the call sites of copy-engine copies (none in a steady-state step)."""
 import collections, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -32,6 +33,15 @@ for cls in (TR.SymmTransport, TR.NcclTransport):
 import torch.distributed as dist
 for n in ["all_reduce", "all_gather_into_tensor", "reduce_scatter_tensor"]:
     wrap(dist, n, "nccl." + n)
+sites = collections.Counter()
+if os.environ.get("COPY_SITES"):  # where the copy-engine copies of the step come from
+    import traceback
+    _ca = K.copy_async
+    def _ca_site(*a, **k):
+        st = traceback.extract_stack(limit=6)[:-1]
+        sites[" <- ".join(f"{os.path.basename(f.filename)}:{f.lineno}" for f in reversed(st[-4:]))] += 1
+        return _ca(*a, **k)
+    K.copy_async = _ca_site
 for _ in range(3):
     step._body()
 torch.cuda.synchronize()
@@ -45,6 +55,8 @@ if comm.rank == 0:
     rows = [(sum(a.elapsed_time(b) for a, b in v), len(v), k) for k, v in recs.items() if v]
     for ms, cnt, k in sorted(rows, reverse=True):
         print(f"  {k:28s} {cnt:4d} calls {ms:8.3f} ms {100 * ms / tot:5.1f}%")
+    for site, cnt in sites.most_common(8):
+        print(f"  copy_async x{cnt // 4}/step: {site}")
 if comm.world_size > 1:
     dist.barrier()
 os._exit(0)
