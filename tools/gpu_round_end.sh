@@ -15,7 +15,7 @@ for n in 2 4; do
   timeout 900 $TR --nproc-per-node $n --master-port $((29800 + n)) bench.py --gpus $n > gpurun_out/${TAG}_b$n.log 2>&1; echo "b$n rc=$?"; line gpurun_out/${TAG}_b$n.log
 done
 t0=$(date +%s); timeout 1200 $TR --nproc-per-node 4 --master-port 29810 bench.py --impl reference --gpus 4 > gpurun_out/${TAG}_ref4.log 2>&1; echo "ref4 rc=$? $(( $(date +%s) - t0 )) s"; grep -c '^{' gpurun_out/${TAG}_ref4.log; line gpurun_out/${TAG}_ref4.log
-timeout 600 python bench.py --config C3 --no-cpu-baseline > gpurun_out/${TAG}_c3_1.log 2>&1; echo "c3 1 rc=$?"; line gpurun_out/${TAG}_c3_1.log
+timeout 600 python bench.py --config C3 --batch 8 --no-cpu-baseline > gpurun_out/${TAG}_c3_1.log 2>&1; echo "c3 1 rc=$?"; line gpurun_out/${TAG}_c3_1.log
 for n in 2 4; do
-  timeout 900 $TR --nproc-per-node $n --master-port $((29820 + n)) bench.py --gpus $n --config C3 > gpurun_out/${TAG}_c3_$n.log 2>&1; echo "c3 $n rc=$?"; line gpurun_out/${TAG}_c3_$n.log
+  timeout 900 $TR --nproc-per-node $n --master-port $((29820 + n)) bench.py --gpus $n --config C3 --batch 8 > gpurun_out/${TAG}_c3_$n.log 2>&1; echo "c3 $n rc=$?"; line gpurun_out/${TAG}_c3_$n.log
 done
