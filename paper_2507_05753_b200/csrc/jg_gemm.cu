@@ -33,6 +33,8 @@ constexpr int BM = 128;
 #define JG_REG_HI 208
 #endif
 constexpr int NUM_EPI_WARPS = JG_EPI_WARPS;  // 8: two per TMEM lane quarter, splitting a tile's column chunks
+static_assert(NUM_EPI_WARPS == 4 || NUM_EPI_WARPS == 8,
+              "epilogue warps: 4 or 8 (12 deadlocks the pipeline and overflows shared memory)");
 constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
 constexpr int SMEM_BUDGET = 196 * 1024;
 
